@@ -1,0 +1,374 @@
+"""Benchmark of the B200 CCQ hot path (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], the Llama-3-8B-shape linears): the MLP-up
+linear d_in 4096 -> d_out 14336 at CCQ 2.06 bits (W2A16), batch M = 1,
+synthetic random_quantized weights (the reference bench's own generator,
+ccq_main.cpp:269-271) and Gaussian bf16 activations.
+
+One step = one decode-GEMV pass over each of L resident layer copies
+(L x 15.3 MB > the 126 MB L2, so every timed launch streams its weights from
+HBM).  value = packed-weight bytes (ccq::model_payload_bytes, kernels.cpp:203)
+moved per second, whole job.  `e2e` is the same metric through the public API
+with host (pinned) activations copied in and outputs copied back each layer.
+
+--impl reference times the reference's own CPU gemv_batch (oracle/_ref,
+compiled from /root/reference) on all host cores, same workload/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CCQ W2A16 GEMV packed-weight GB/s (% HBM peak); GEMM TFLOP/s at batch 1-256"
+D_IN, D_OUT, FAMILY, M_HEAD = 4096, 14336, 2, 1
+SEED = 4096 * 31 + 14336  # ccq_main.cpp:269-271 seeding: seed + d_in*31 + d_out (seed 0)
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([v.strip() for v in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl != "reference" else "gloo")
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    """The reference CPU path (oracle/_ref), all host threads, bounded sample."""
+    if rank != 0:
+        return None
+    import numpy as np
+    import oracle as O
+    threads = os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    x = O.random_matrix(M_HEAD, D_IN, "gaussian", SEED + 1)
+    if kind == "reference":
+        model = O.RefModel.random(D_OUT, D_IN, FAMILY, 64, SEED)
+        payload = model.payload_bytes()
+        runner = O.RefSharded(model, threads)
+        call = lambda: runner.gemv_batch(x)  # noqa: E731
+    else:
+        s = O.random_packed(D_OUT, D_IN, FAMILY, 64, SEED)
+        payload = O.payload_bytes(s)
+        call = lambda: O.gemv_batch(s, x, threads=threads)  # noqa: E731
+    for _ in range(args.warmup):
+        call()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    dt = (time.perf_counter() - t0) / args.steps
+    gbs = payload / dt / 1e9
+    sample = f"{args.steps} x gemv_batch 4096x14336 2.06 M=1 ({threads} threads, row-sharded)"
+    return {"metric": METRIC, "value": gbs, "unit": "GB/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (random_quantized, Gaussian x)",
+            "config": {"workload": "configs[1] Llama-3-8B MLP-up linear 4096->14336, CCQ 2.06, M=1",
+                       "d_in": D_IN, "d_out": D_OUT, "family": "2.06", "batch": M_HEAD},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline_leg():
+    """Reference CPU path timed on this host (rank 0, N=1 only), ~10 s."""
+    import oracle as O
+    threads = os.cpu_count() or 1
+    x = O.random_matrix(M_HEAD, D_IN, "gaussian", SEED + 1)
+    if O.ref_available():
+        model = O.RefModel.random(D_OUT, D_IN, FAMILY, 64, SEED)
+        payload, kind = model.payload_bytes(), "reference"
+        runner = O.RefSharded(model, threads)
+        call = lambda: runner.gemv_batch(x)  # noqa: E731
+    else:
+        s = O.random_packed(D_OUT, D_IN, FAMILY, 64, SEED)
+        payload, kind = O.payload_bytes(s), "port"
+        call = lambda: O.gemv_batch(s, x, threads=threads)  # noqa: E731
+    call()
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < 8.0 or n < 3:
+        call()
+        n += 1
+    dt = (time.perf_counter() - t0) / n
+    return {"value": payload / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{n} x gemv_batch 4096x14336 2.06 M=1 on {threads} threads "
+                      f"({dt*1e3:.1f} ms each)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ccq", choices=["ccq", "reference"])
+    ap.add_argument("--layers", type=int, default=12)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="add an M / family sweep")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local = dist_init(args)
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out))
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2507_07145_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+
+    # --- synthetic layers: L resident copies (different seeds) -------------
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    layers = []
+    for l in range(args.layers):
+        s = _synthetic(D_OUT, D_IN, FAMILY, 64, SEED + 1000 * l + rank)
+        layers.append(P.DeviceModel.upload(s, device=local))
+    payload = layers[0].payload_bytes
+    gen = torch.Generator(device="cpu").manual_seed(SEED + rank)
+    x_host = torch.randn(args.layers, M_HEAD, D_IN, generator=gen).to(torch.bfloat16).pin_memory()
+    x_dev = x_host.to(dev)
+    y_dev = torch.empty(args.layers, M_HEAD, D_OUT, dtype=torch.float32, device=dev)
+    y_host = torch.empty_like(y_dev, device="cpu").pin_memory()
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for l in range(args.layers):
+            P.matmul(layers[l], x_dev[l], out=y_dev[l], stream=stream)
+
+    # capture one step in a CUDA graph (launch-bound inner loop)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            step()
+    stream.synchronize()
+    n0 = P.launch_count()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    kernels_per_step = P.launch_count() - n0
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    bytes_step = payload * args.layers
+    value = bytes_step * world / (ms * 1e-3) / 1e9
+    per_launch_us = ms * 1e3 / args.layers
+    alg_bytes = payload + M_HEAD * D_IN * 2 + M_HEAD * D_OUT * 4
+    achieved = alg_bytes / (per_launch_us * 1e-6) / 1e9
+
+    # --- e2e: public API, host activations in, outputs back, every layer ----
+    def e2e_step():
+        for l in range(args.layers):
+            x_dev[l].copy_(x_host[l], non_blocking=True)
+            P.matmul(layers[l], x_dev[l], out=y_dev[l], stream=stream)
+            y_host[l].copy_(y_dev[l], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            e2e_step()
+    stream.synchronize()
+    barrier()
+    with torch.cuda.stream(stream):
+        start.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = bytes_step * world / (e2e_ms * 1e-3) / 1e9
+
+    sweep = None
+    if args.sweep and rank == 0:
+        sweep = run_sweep(P, torch, dev, stream, hbm_peak)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg()
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic: random_quantized CCQ 2.06 weights (synthetic.cpp:25-103), "
+                    "Gaussian bf16 activations",
+            "config": {"workload": "configs[1] Llama-3-8B MLP-up linear d_in 4096 -> d_out 14336, "
+                                   "CCQ 2.06 (W2A16), batch M=1",
+                       "d_in": D_IN, "d_out": D_OUT, "family": "2.06", "batch": M_HEAD,
+                       "layers_per_step": args.layers,
+                       "l2": f"inputs larger than L2: {args.layers} resident layer copies = "
+                             f"{bytes_step/1e6:.0f} MB rotated per step",
+                       "parallelism": f"replicas x{world}"},
+            "hbm_fraction": value / world / hbm_peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "gemv_stream<2.06,RPW=4,MT=1>",
+                         "per_launch_us": per_launch_us, "alg_bytes_per_launch": alg_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
+                         else "fallback 6650 GB/s (B200_PROFILING.md)"},
+            "e2e": {"value": e2e_val, "unit": "GB/s",
+                    "h2d_bytes_per_step": args.layers * M_HEAD * D_IN * 2,
+                    "d2h_bytes_per_step": args.layers * M_HEAD * D_OUT * 4,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": kernels_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+        if sweep is not None:
+            out["sweep"] = sweep
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_sweep(P, torch, dev, stream, hbm_peak):
+    """Packed GB/s and TFLOP/s per (family, shape, M) - graph-timed, L2-cold."""
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    res = []
+    shapes = [(4096, 14336), (14336, 4096), (4096, 4096)]
+    for fam, fname in ((2, "2.06"), (1, "2.5"), (0, "2.75")):
+        for (din, dout) in shapes:
+            copies = max(2, int(160e6 // (din * dout * 0.35)) + 1)
+            ms_ = [P.DeviceModel.upload(_synthetic(dout, din, fam, 64, 17 + c), device=dev.index)
+                   for c in range(copies)]
+            pb = ms_[0].payload_bytes
+            for M in (1, 2, 4, 8, 16):
+                x = torch.randn(M, din, device=dev).to(torch.bfloat16)
+                y = torch.empty(M, dout, device=dev)
+                def body():
+                    for mm in ms_:
+                        P.matmul(mm, x, out=y, stream=stream)
+                with torch.cuda.stream(stream):
+                    body()
+                stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    body()
+                for _ in range(3):
+                    g.replay()
+                torch.cuda.synchronize()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 20
+                with torch.cuda.stream(stream):
+                    s0.record(stream)
+                    for _ in range(reps):
+                        g.replay()
+                    s1.record(stream)
+                torch.cuda.synchronize()
+                us = s0.elapsed_time(s1) * 1e3 / (reps * copies)
+                res.append({"family": fname, "d_in": din, "d_out": dout, "M": M,
+                            "us": round(us, 3), "packed_GBps": round(pb / us / 1e3, 1),
+                            "hbm_frac": round(pb / us / 1e3 / hbm_peak, 4),
+                            "TFLOPs": round(2 * M * din * dout / us / 1e6, 3)})
+            del ms_
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+"""GPU parity: the sm_100a kernels against the CPU oracle on the same inputs.
+
+Bar (BASELINE.json north_star): decoded levels and dequantized weights are
+bit-exact; matmul outputs are within relative Frobenius error 1e-3 (fp32
+accumulation vs the reference's double accumulation).  We assert a much
+tighter REL_TOL so regressions show up long before the contract bound.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+CONTRACT_TOL = 1e-3  # north_star: rel. err <= 1e-3
+REL_TOL = 2e-5       # what the kernels actually achieve (fp32 accumulate)
+
+
+def rel_err(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    den = np.sqrt((want * want).sum())
+    num = np.sqrt(((got - want) ** 2).sum())
+    return num if den == 0 else num / den
+
+
+def bf16_round(x):
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
+SHAPES = [(1, 64), (8, 128), (33, 192), (96, 128), (257, 4096), (130, 14336), (5, 2048 + 64)]
+
+
+@pytest.fixture(scope="module")
+def models(oracle, ccq, cuda):
+    out = {}
+    for fam in (0, 1, 2):
+        for (rows, cols) in SHAPES:
+            s = oracle.random_packed(rows, cols, fam, 64, seed=rows * 31 + cols + fam)
+            out[(fam, rows, cols)] = (s, ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s)))
+    return out
+
+
+# ---------------------------------------------------------------- decode (a) --
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_decode_bit_exact(models, oracle, ccq, cuda, fam, shape):
+    torch = cuda
+    s, d = models[(fam, *shape)]
+    lv = torch.empty(shape, dtype=torch.int8, device="cuda")
+    w = torch.empty(shape, dtype=torch.float32, device="cuda")
+    ccq.decode(d, levels=lv, weights=w)
+    torch.cuda.synchronize()
+    assert np.array_equal(lv.cpu().numpy(), oracle.levels(s))
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), oracle.dequantize(s).view(np.uint32))
+
+
+@pytest.mark.parametrize("fam,gs", [(0, 66), (2, 65), (1, 57), (0, 64), (2, 64)])
+def test_decode_non_default_geometry(oracle, ccq, cuda, fam, gs):
+    torch = cuda
+    s = oracle.random_packed(9, gs * 5, fam, gs, seed=gs + fam)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    lv = torch.empty(9, gs * 5, dtype=torch.int8, device="cuda")
+    w = torch.empty(9, gs * 5, dtype=torch.float32, device="cuda")
+    ccq.decode(d, levels=lv, weights=w)
+    assert np.array_equal(lv.cpu().numpy(), oracle.levels(s))
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), oracle.dequantize(s).view(np.uint32))
+    # generic GEMV path for non-64 group sizes
+    x = oracle.random_matrix(3, gs * 5, "gaussian", 4)
+    y = ccq.gemv_batch(d, x)
+    assert rel_err(y, oracle.gemv_batch(s, x)) < REL_TOL
+
+
+@pytest.mark.parametrize("name", ["2.75", "2.5", "2.06"])
+def test_acceptance_fixture_decode(oracle, ccq, cuda, name):
+    """Criterion 6 on the GPU: the reference-written container decodes
+    bit-identically to the reference's quantizer reconstruction."""
+    import hashlib
+    import json
+    gold = json.load(open(os.path.join(GOLDEN, "golden.json")))["acceptance"][name]
+    path = os.path.join(GOLDEN, f"acc512_{name}.ccq")
+    d = ccq.DeviceModel.load(path)
+    deq = ccq.dequantize(d)
+    assert hashlib.sha256(deq.tobytes()).hexdigest() == gold["recon_sha"]
+    ref = np.load(os.path.join(GOLDEN, f"acc512_{name}.npz"))
+    y = ccq.gemv_batch(d, ref["x"])
+    assert rel_err(y, ref["y"]) < REL_TOL
+
+
+def test_dequantize_host_matches_oracle(models, oracle, ccq):
+    for fam in (0, 1, 2):
+        s, d = models[(fam, 257, 4096)]
+        assert np.array_equal(ccq.dequantize(d).view(np.uint32), oracle.dequantize(s).view(np.uint32))
+
+
+def test_zero_scale_codes_decode_to_zero(oracle, ccq, cuda):
+    # test_kernels.cpp:89-101
+    for fam in (0, 1, 2):
+        s = oracle.random_packed(4, 128, fam, 64, 21)
+        if fam == 2:
+            s.scale_payload[:] = 0
+        else:
+            codes = s.code_payload.reshape(-1, 22 if fam == 0 else 20)
+            if fam == 0:
+                codes[:, 21] &= 0xF0
+            else:
+                codes[:, 18] = 0
+                codes[:, 19] &= 0xE0
+        d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+        assert (ccq.dequantize(d) == 0).all()
+        assert (ccq.gemv_batch(d, oracle.random_matrix(2, 128, "gaussian", 1)) == 0).all()
+
+
+# ------------------------------------------------------------------ gemv (b) --
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 5])
+def test_gemv_f32_matches_oracle(models, oracle, ccq, cuda, fam, shape, M):
+    s, d = models[(fam, *shape)]
+    x = oracle.random_matrix(M, shape[1], "gaussian", 1000 + M)
+    y = ccq.gemv_batch(d, x)
+    want = oracle.gemv_batch(s, x, threads=8)
+    err = rel_err(y, want)
+    assert err < REL_TOL, err
+    assert err < CONTRACT_TOL
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+@pytest.mark.parametrize("M", [1, 2, 4, 8, 16])
+def test_gemv_bf16_device(models, oracle, ccq, cuda, fam, M):
+    torch = cuda
+    s, d = models[(fam, 130, 14336)]
+    x = oracle.random_matrix(M, 14336, "gaussian", 7 + M)
+    xb = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+    y = ccq.matmul(d, xb, kernel="gemv")
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, bf16_round(x), threads=8)  # oracle fed the same bf16 x
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
+
+
+def test_gemv_single_vector_and_shape_errors(models, oracle, ccq):
+    s, d = models[(0, 33, 192)]
+    x = oracle.random_matrix(1, 192, "uniform", 99)[0]
+    assert rel_err(ccq.gemv(d, x), oracle.gemv_batch(s, x)[0]) < REL_TOL
+    # test_kernels.cpp:151-161
+    with pytest.raises(ccq.ShapeError):
+        ccq.gemv(d, np.zeros(191, np.float32))
+    with pytest.raises(ccq.ShapeError):
+        ccq.gemv(d, np.zeros(192, np.float32), np.zeros(32, np.float32))
+    with pytest.raises(ccq.ShapeError):
+        ccq.gemv_batch(d, np.zeros((2, 192), np.float32), np.zeros((3, 33), np.float32))
+    with pytest.raises(ccq.ShapeError):
+        ccq.gemv_batch(d, np.zeros((2, 192), np.float32), np.zeros((2, 34), np.float32))
+
+
+def test_gemv_zero_vector_and_linearity(models, oracle, ccq):
+    # test_kernels.cpp:117-137
+    s, d = models[(1, 96, 128)]
+    assert (ccq.gemv(d, np.zeros(128, np.float32)) == 0).all()
+    a = oracle.random_matrix(1, 128, "gaussian", 1)[0]
+    b = oracle.random_matrix(1, 128, "gaussian", 2)[0]
+    ya, yb, yab = ccq.gemv(d, a), ccq.gemv(d, b), ccq.gemv(d, 2 * a + b)
+    assert rel_err(yab, 2 * ya + yb) < 1e-5
+
+
+def test_widening_domain_error_on_upload(oracle, ccq, cuda):
+    """A stored byte whose widened code leaves [0, 2^15) raises DomainError
+    (the reference raises the same error when decoding it, coding.hpp:145)."""
+    s = oracle.random_packed(4, 128, 2, 64, 3)
+    s.cluster_scales[1] = np.float32(200.0)
+    s.cluster_zero_points[1] = np.float32(0.0)
+    s.code_payload[32 * 1 + 5] = 255  # row 1 (32 bytes per row) gets q = 255 -> 51000
+    with pytest.raises(ccq.DomainError):
+        ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    # the same parameters are accepted when no such byte is stored
+    s.code_payload[32:64] = np.minimum(s.code_payload[32:64], 100)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    assert np.array_equal(ccq.dequantize(d).view(np.uint32), oracle.dequantize(s).view(np.uint32))
+
+
+def test_widening_plans_exhaustive_random_rows(oracle, ccq, cuda):
+    """Every q of many random (alpha, beta) rows, including tiny/huge alpha and
+    exact-tie values, widens exactly as lround(q*alpha+beta)."""
+    rng = np.random.default_rng(1)
+    rows = 512
+    s = oracle.random_packed(rows, 256, 2, 64, 5)
+    alphas = np.concatenate([1 + rng.random(rows - 8) * 64, [2.5, 0.5, 1.0, 0.25, 1e-3, 127.9, 128.49, 3.0]])
+    s.cluster_scales[:] = alphas.astype(np.float32)
+    for r in range(rows):
+        a = float(s.cluster_scales[r])
+        s.cluster_zero_points[r] = np.float32(rng.random() * max(0.0, 32767 - 255 * a - 1))
+    s.cluster_zero_points[-8:] = np.float32([0.5, 0.25, 7.0, 0.0, 3.5, 0.0, 0.0, 1.5])
+    # every q appears in every row: bytes 0..255 (rows are 256 bytes wide)
+    s.code_payload[:] = np.tile(np.arange(256, dtype=np.uint8), rows)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    assert np.array_equal(ccq.dequantize(d).view(np.uint32), oracle.dequantize(s).view(np.uint32))
+
+
+def test_row_sharded_upload_concatenates(oracle, ccq, cuda):
+    s = oracle.random_packed(64, 512, 2, 64, 8)
+    pm = ccq.PackedModel.from_sections(s)
+    x = oracle.random_matrix(2, 512, "gaussian", 3)
+    parts = [ccq.DeviceModel.upload(pm, rows=(r, r + 16)) for r in range(0, 64, 16)]
+    y = np.concatenate([ccq.gemv_batch(p, x) for p in parts], axis=1)
+    assert rel_err(y, oracle.gemv_batch(s, x)) < REL_TOL
+    deq = np.concatenate([ccq.dequantize(p) for p in parts], axis=0)
+    assert np.array_equal(deq.view(np.uint32), oracle.dequantize(s).view(np.uint32))
+
+
+def test_empty_inputs(oracle, ccq, cuda):
+    s = oracle.random_packed(0, 128, 0, 64, 1)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    assert ccq.dequantize(d).shape == (0, 128)
+    s = oracle.random_packed(4, 128, 1, 64, 1)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    assert ccq.gemv_batch(d, np.zeros((0, 128), np.float32)).shape == (0, 4)
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_baseline_shape_full_size(oracle, ccq, cuda, fam):
+    """BASELINE config 2 shape (d_in 4096 -> d_out 14336) at full size, M=1,
+    against the (multithreaded) oracle."""
+    s = oracle.random_packed(14336, 4096, fam, 64, seed=4096 * 31 + 14336)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = oracle.random_matrix(1, 4096, "gaussian", 4096 + 1)
+    y = ccq.gemv_batch(d, x)
+    assert rel_err(y, oracle.gemv_batch(s, x, threads=8)) < REL_TOL
