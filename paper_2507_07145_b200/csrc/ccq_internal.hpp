@@ -1,17 +1,20 @@
 // Internal definitions shared by the CCQ sm_100a kernels and the C ABI.
 //
-// Device layout of an uploaded model:
-//   codes    rows x code_stride bytes; row r holds its groups exactly as in
-//            the reference's group-major code_payload (container.hpp:44),
-//            padded to a 16-byte row stride so every row (and every 32-group
-//            chunk at group size 64) starts on a 16-byte boundary for
-//            cp.async.bulk / 128-bit loads.
-//   nibbles  side-band scale nibbles re-laid out per row (row r starts at
-//            byte r*nib_stride; group gj of the row in the low nibble of
-//            byte gj/2 when gj is even), stride padded to 16 bytes.
-//   super    f32[rows]   per-row super scale (FORMAT.md §5)
-//   plan     WidenPlan[rows] (2.06 only): the exact fixed-point restatement of
-//            clustered_code_value (coding.hpp:142-150), see widen() below.
+// Device layout of an uploaded model, "chunk-major":
+//   K is cut into nch chunks of kChunk = 32 groups.  The reference stores
+//   codes group-major per row (container.hpp:44); on the device
+//     codes    [nch][rows][cgb]   cgb = round_up(32 * payload_bytes, 16)
+//              chunk c of row r holds groups 32c .. 32c+31 of the row,
+//              byte-identical to the reference payload of those groups;
+//     nibbles  [nch][rows][16]    side-band scale nibbles of the same 32
+//              groups (group j of the chunk in the low nibble of byte j/2
+//              when j is even), side-band families only;
+//     super    f32[rows]          per-row super scale (FORMAT.md §5);
+//     plan     WidenPlan[rows]    (2.06 only) exact fixed-point restatement
+//              of clustered_code_value (coding.hpp:142-150), see below.
+//   A warp working on chunk c of consecutive rows therefore reads ONE
+//   contiguous region per tile (one bulk copy each for codes, nibbles,
+//   plans).  Every chunk row starts 16-byte aligned.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -46,23 +49,56 @@ struct Geometry {
 };
 
 // Exact fixed-point widening plan of one row (2.06).  For every stored byte q
-// that can occur,
-//     hi = (uint32)(( (uint64)(q << sh) * M + C ) >> 32)
+// that can occur, with q placed in byte `pos` of a 32-bit word,
+//     hi = (uint32)(( (uint64)(q << 8*pos) * M + C ) >> 32)
 // satisfies  hi >> 8 == lround(double(q)*alpha + double(beta))  and
 // hi < 2^23, i.e. hi carries the 15-bit code at bits [8,23) with 8 fraction
-// bits below.  M = alpha * 2^(40-sh) is an exact integer (alpha is an f32),
-// C = floor((beta + 0.5) * 2^40); the host builder verifies all 256 q
+// bits below.  M = alpha * 2^(40-8*pos) is an exact integer (alpha is an
+// f32), C = floor((beta + 0.5) * 2^40); the host builder verifies all 256 q
 // against the reference double formula (model.cu: build_widen_plan).
+// On the device the 64-bit multiply-add is ONE IMAD.HI.U32 (64-bit addend).
+//   sel: bits 0-15  PRMT selector moving byte 0 of a word to byte `pos`
+//                   (zeros elsewhere);
+//        bits 16-31 1 << (4*pos): adding b * that selects byte b instead.
 struct __align__(16) WidenPlan {
   uint64_t C;
   uint32_t M;
-  uint32_t sh;  // 0, 8, 16 or 24
+  uint32_t sel;
 };
 
+__host__ __device__ constexpr uint32_t plan_sel(uint32_t pos) {
+  return ((0x4444u & ~(0xFu << (4 * pos))) & 0xFFFFu) | ((1u << (4 * pos)) << 16);
+}
+__host__ __device__ __forceinline__ uint32_t plan_pos(const WidenPlan& p) {
+  const uint32_t step = p.sel >> 16;
+  return step == 1 ? 0 : step == 16 ? 1 : step == 256 ? 2 : 3;
+}
 __host__ __device__ __forceinline__ uint32_t widen_hi(uint32_t q, const WidenPlan& p) {
-  const uint64_t v = uint64_t(q << p.sh) * uint64_t(p.M) + p.C;
+  const uint64_t v = uint64_t(q << (8 * plan_pos(p))) * uint64_t(p.M) + p.C;
   return uint32_t(v >> 32);
 }
+
+constexpr int kChunk = 32;  // groups per K-chunk in the device layout
+
+// Read-only view of the device layout, passed to kernels by value.
+struct DevLayout {
+  const uint8_t* codes;
+  const uint8_t* nibbles;
+  const float* super;
+  const WidenPlan* plan;
+  int64_t rows, cols, gpr;
+  uint32_t cgb;  // bytes per (chunk, row)
+  int nch;
+  Geometry geo;
+
+  __host__ __device__ __forceinline__ const uint8_t* group(int64_t r, int64_t gj) const {
+    return codes + (uint64_t(gj / kChunk) * rows + r) * cgb + (gj % kChunk) * geo.payload_bytes;
+  }
+  __host__ __device__ __forceinline__ uint32_t nibble(int64_t r, int64_t gj) const {
+    const uint8_t b = nibbles[(uint64_t(gj / kChunk) * rows + r) * 16 + (gj % kChunk) / 2];
+    return (b >> (4 * (gj & 1))) & 0xFu;
+  }
+};
 
 }  // namespace ccqb
 
@@ -76,17 +112,22 @@ struct ccq_dev_model {
   void* base = nullptr;
   size_t device_bytes = 0;
   uint8_t* codes = nullptr;
-  uint64_t code_stride = 0;
   uint8_t* nibbles = nullptr;
-  uint64_t nib_stride = 0;
   float* super = nullptr;
   ccqb::WidenPlan* plan = nullptr;
+  uint32_t cgb = 0;  // bytes per (chunk, row)
+  int nch = 0;       // K chunks
 
   uint64_t payload_bytes = 0;  // model_payload_bytes of the reference model
   bool fast = false;           // group-64 streaming kernels apply
 };
 
 namespace ccqb {
+
+inline DevLayout layout_of(const ccq_dev_model* m) {
+  return DevLayout{m->codes, m->nibbles, m->super, m->plan, m->rows, m->cols, m->gpr,
+                   m->cgb, m->nch, m->geo};
+}
 
 // Thread-local error message + status helpers.
 void set_error(const std::string& msg);

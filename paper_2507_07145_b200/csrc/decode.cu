@@ -19,15 +19,10 @@ namespace ccqb {
 namespace {
 
 struct DecodeArgs {
-  const uint8_t* codes;
-  const uint8_t* nibbles;
-  const float* super;
-  const WidenPlan* plan;
+  DevLayout L;
   int8_t* levels;
   float* weights;
-  int64_t rows, cols, gpr, groups;
-  uint64_t code_stride, nib_stride;
-  Geometry geo;
+  int64_t groups;
 };
 
 template <int FAM>
@@ -43,23 +38,24 @@ __global__ void __launch_bounds__(256) decode_generic(DecodeArgs a) {
   constexpr FamilyConst fc = family_const(FAM);
   const int64_t gi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gi >= a.groups) return;
-  const int64_t r = gi / a.gpr, gj = gi - r * a.gpr;
-  const uint8_t* p = a.codes + r * a.code_stride + gj * a.geo.payload_bytes;
+  const DevLayout& L = a.L;
+  const int64_t r = gi / L.gpr, gj = gi - r * L.gpr;
+  const uint8_t* p = L.group(r, gj);
   uint32_t sc;
-  if (a.geo.embedded_scale) {
-    sc = load_word<FAM>(p + a.geo.full_words * fc.word_bytes) & fc.scale_mask;
+  if (L.geo.embedded_scale) {
+    sc = load_word<FAM>(p + L.geo.full_words * fc.word_bytes) & fc.scale_mask;
   } else {
-    sc = (a.nibbles[r * a.nib_stride + gj / 2] >> (4 * (gj & 1))) & 0xF;
+    sc = L.nibble(r, gj);
   }
-  const float scale = __fmul_rn(float(sc), a.super[r]);
+  const float scale = __fmul_rn(float(sc), L.super[r]);
   WidenPlan pl{};
-  if constexpr (fc.cluster) pl = a.plan[r];
-  const int64_t base = r * a.cols + gj * a.geo.group_size;
+  if constexpr (fc.cluster) pl = L.plan[r];
+  const int64_t base = r * L.cols + gj * L.geo.group_size;
   int idx = 0;
-  for (int w = 0; w < a.geo.words_per_group; ++w) {
+  for (int w = 0; w < L.geo.words_per_group; ++w) {
     uint32_t code = load_word<FAM>(p + w * fc.word_bytes);
     if constexpr (fc.cluster) code = widen_hi(code, pl) >> 8;
-    const int nk = (w < a.geo.full_words) ? fc.wpw : 1;
+    const int nk = (w < L.geo.full_words) ? fc.wpw : 1;
     for (int k = 0; k < nk; ++k) {
       const int lv = int((code >> fc.shifts[k]) & fc.weight_mask) - fc.zero_point;
       if (a.weights) a.weights[base + idx] = __fmul_rn(float(lv), scale);
@@ -76,8 +72,9 @@ __global__ void __launch_bounds__(128) decode_g64(DecodeArgs a) {
   constexpr FamilyConst fc = family_const(FAM);
   const int64_t gi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gi >= a.groups) return;
-  const int64_t r = gi / a.gpr, gj = gi - r * a.gpr;
-  const uint8_t* p = a.codes + r * a.code_stride + gj * a.geo.payload_bytes;
+  const DevLayout& L = a.L;
+  const int64_t r = gi / L.gpr, gj = gi - r * L.gpr;
+  const uint8_t* p = L.group(r, gj);
 
   // Stored words of the group, widened to code values.
   uint32_t code[22];
@@ -85,10 +82,10 @@ __global__ void __launch_bounds__(128) decode_g64(DecodeArgs a) {
   if constexpr (FAM == kF206) {
     const uint4 v = *reinterpret_cast<const uint4*>(p);
     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-    const WidenPlan pl = a.plan[r];
+    const WidenPlan pl = L.plan[r];
 #pragma unroll
     for (int i = 0; i < 16; ++i) code[i] = widen_hi((wv[i / 4] >> (8 * (i % 4))) & 0xFF, pl) >> 8;
-    sc = (a.nibbles[r * a.nib_stride + gj / 2] >> (4 * (gj & 1))) & 0xF;
+    sc = L.nibble(r, gj);
   } else if constexpr (FAM == kF25) {
     const uint32_t* p32 = reinterpret_cast<const uint32_t*>(p);  // 20 B, 4-B aligned
 #pragma unroll
@@ -108,7 +105,7 @@ __global__ void __launch_bounds__(128) decode_g64(DecodeArgs a) {
     }
     sc = code[21] & fc.scale_mask;
   }
-  const float scale = __fmul_rn(float(sc), a.super[r]);
+  const float scale = __fmul_rn(float(sc), L.super[r]);
 
   int lv[64];
 #pragma unroll
@@ -142,8 +139,7 @@ __global__ void __launch_bounds__(128) decode_g64(DecodeArgs a) {
 
 template <int FAM>
 int launch_fam(const ccq_dev_model* m, int8_t* levels, float* weights, cudaStream_t s) {
-  DecodeArgs a{m->codes, m->nibbles, m->super, m->plan, levels, weights, m->rows, m->cols,
-               m->gpr, m->rows * m->gpr, m->code_stride, m->nib_stride, m->geo};
+  DecodeArgs a{layout_of(m), levels, weights, m->rows * m->gpr};
   if (a.groups == 0) return CCQ_OK;
   const bool aligned = (reinterpret_cast<uintptr_t>(levels) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(weights) % 16 == 0);

@@ -6,19 +6,21 @@
 // in f32 (tolerance parity).
 //
 // Streaming structure (group size 64, the BASELINE shapes):
-//   * persistent CTAs (one per SM), 8-16 warps each;
-//   * activations x[M][K] are staged once per CTA in shared memory as f32,
-//     in a per-family permuted order so every FFMA2 operand pair is a
-//     naturally aligned float2, together with one correction term Q per
-//     (token, group);
-//   * each warp owns whole row tiles (RPW rows x all of K) and streams them
-//     through its own S-stage shared-memory ring filled by 1-D bulk copies
-//     (cp.async.bulk, the TMA engine) with mbarrier completion - no register
-//     cost for bytes in flight and no block-wide barriers in the main loop;
-//   * lane l decodes group (32c + l) of every row of the tile, so one load of
-//     its 64 activations serves RPW rows;
-//   * partial sums are reduced with warp shuffles; y is written once per
-//     (row, token) - deterministic, no atomics.
+//   * persistent CTAs (one per SM); CTA i owns the contiguous output rows
+//     [i*rows/G, (i+1)*rows/G) - balanced to one row;
+//   * K is cut into nch chunks of CG <= 32 groups; warp w works on chunk
+//     w % nch for the row "stream" w / nch.  Lane l owns group c*CG + l for
+//     the whole kernel, so its 64 activations (f32, permuted per family so
+//     every FFMA2 operand pair is an aligned register pair) and the group's
+//     correction term Q are loaded into REGISTERS once (M = 1): no shared
+//     memory traffic for x at all.  For M > 1, x is staged in shared memory.
+//   * each warp streams its rows (RPW-row tiles, interleaved across streams)
+//     through its own S-stage shared-memory ring, filled by 1-D bulk copies
+//     (cp.async.bulk on the TMA engine) with mbarrier completion: no
+//     register cost for bytes in flight, no block barriers in the main loop;
+//   * per-(row, chunk) partials are reduced with warp shuffles into shared
+//     memory and summed over chunks in a fixed order at the end: y is
+//     written once per (row, token) - deterministic, no atomics.
 //
 // Decode arithmetic (per stored word, no lookup tables):
 //   each state field is masked into the top mantissa bits of 1.0f
@@ -120,21 +122,25 @@ struct G64<kF25> {
   __host__ __device__ static bool exact_tail(int i) { return i == 63; }
 };
 
+
+// (v & MASK) | one in ONE LOP3: `one` lives in a register (a second
+// immediate would make the compiler split the op in two).
+template <uint32_t MASK>
+__device__ __forceinline__ float fm(uint32_t v, uint32_t one) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(v), "n"(MASK), "r"(one));
+  return __uint_as_float(d);
+}
+
 struct GemvArgs {
-  const uint8_t* codes;
-  const uint8_t* nibbles;
-  const float* super;
-  const WidenPlan* plan;
+  DevLayout L;
   const void* x;
   void* y;
   int x_dtype, y_dtype;
-  int64_t rows, cols, gpr;
-  uint64_t code_stride, nib_stride;
-  int M;  // tokens handled by this launch (<= MT)
+  int M;                       // tokens handled by this launch (<= MT)
   int64_t x_stride, y_stride;  // elements between token rows
-  int64_t tiles;
-  int nchunks;
-  int stages;
+  int streams;                 // row streams per CTA (warps = nch * streams)
+  int rows_per_cta_max;
 };
 
 __device__ __forceinline__ float load_x(const void* x, int dtype, int64_t i) {
@@ -144,215 +150,191 @@ __device__ __forceinline__ float load_x(const void* x, int dtype, int64_t i) {
   return __half2float(__ushort_as_half(h));
 }
 
+// Activations of one group, permuted: either a register copy (M = 1) or a
+// pointer into shared memory.
+template <int FAM, bool REG>
+struct XGroup;
+template <int FAM>
+struct XGroup<FAM, true> {
+  float4 v[G64<FAM>::XG / 4];
+  __device__ __forceinline__ float4 f4(int k) const { return v[k]; }
+};
+template <int FAM>
+struct XGroup<FAM, false> {
+  const float* p;
+  __device__ __forceinline__ float4 f4(int k) const {
+    return *reinterpret_cast<const float4*>(p + 4 * k);
+  }
+};
+
 // ---------------------------------------------------------------------------
-// Per-family group consumers.  Each returns nothing; they accumulate the
-// group's  sum (s - zp) * x  (unscaled) into dot[r][m] for RPW rows.
+// Group decoders: return  sum_i (s_i - zp) * x_i  for one group (unscaled),
+// given the group's payload in shared memory.
 // ---------------------------------------------------------------------------
 
-template <int RPW, int MT>
-__device__ __forceinline__ void consume_206(const uint8_t* stage, int lane, const float* xs,
-                                            const float* qs, int64_t gstride_x, int64_t qstride,
-                                            const WidenPlan (&pl)[RPW], const uint32_t (&sel)[RPW][4],
-                                            const float (&scf)[RPW], float (&acc)[RPW][MT]) {
-  constexpr int CHB = 32 * 16;
-  uint4 c[RPW];
-#pragma unroll
-  for (int r = 0; r < RPW; ++r) c[r] = lds128(stage + r * (CHB + 16) + lane * 16);
-  float2 a[RPW][MT];
-#pragma unroll
-  for (int r = 0; r < RPW; ++r)
-#pragma unroll
-    for (int m = 0; m < MT; ++m) a[r][m] = make_float2(0.f, 0.f);
+// 2.06: 16 clustered bytes.
+template <class X>
+__device__ __forceinline__ float dot_206(const uint8_t* gp, const X& x, float q,
+                                         const WidenPlan& pl, const uint32_t (&sel)[4],
+                                         uint32_t one) {
+  const uint4 c = lds128(gp);
+  float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int wi = 0; wi < 4; ++wi) {
-    float4 xv[MT][4];
+    const uint32_t word = wi == 0 ? c.x : wi == 1 ? c.y : wi == 2 ? c.z : c.w;
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        xv[m][k] = *reinterpret_cast<const float4*>(xs + m * gstride_x + wi * 16 + 4 * k);
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const uint32_t word = wi == 0 ? c[r].x : wi == 1 ? c[r].y : wi == 2 ? c[r].z : c[r].w;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t q = prmt(word, 0u, sel[r][b]);
-        const uint32_t hi = uint32_t((uint64_t(q) * pl[r].M + pl[r].C) >> 32);
-        const uint32_t h2 = hi << 6;
-        const float2 f01 = make_float2(as_f((hi & 0x007E0000u) | kOne), as_f((hi & 0x000FC000u) | kOne));
-        const float2 f23 = make_float2(as_f((h2 & 0x007E0000u) | kOne), as_f((h2 & 0x000FC000u) | kOne));
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          const float4 xx = xv[m][b];
-          a[r][m] = __ffma2_rn(f01, make_float2(xx.x, xx.y), a[r][m]);
-          a[r][m] = __ffma2_rn(f23, make_float2(xx.z, xx.w), a[r][m]);
-        }
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t qb = prmt(word, 0u, sel[b]);
+      const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);
+      const uint32_t h2 = hi << 6;
+      const float2 f01 = make_float2(fm<0x007E0000u>(hi, one), fm<0x000FC000u>(hi, one));
+      const float2 f23 = make_float2(fm<0x007E0000u>(h2, one), fm<0x000FC000u>(h2, one));
+      const float4 xx = x.f4(4 * wi + b);
+      if (b & 1) {
+        a1 = __ffma2_rn(f01, make_float2(xx.x, xx.y), a1);
+        a1 = __ffma2_rn(f23, make_float2(xx.z, xx.w), a1);
+      } else {
+        a0 = __ffma2_rn(f01, make_float2(xx.x, xx.y), a0);
+        a0 = __ffma2_rn(f23, make_float2(xx.z, xx.w), a0);
       }
     }
   }
-#pragma unroll
-  for (int m = 0; m < MT; ++m) {
-    const float q = qs[m * qstride];
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const float dot = fmaf(64.f, a[r][m].x, fmaf(512.f, a[r][m].y, -q));
-      acc[r][m] = fmaf(scf[r], dot, acc[r][m]);
-    }
-  }
+  return fmaf(64.f, a0.x + a1.x, fmaf(512.f, a0.y + a1.y, -q));
 }
 
-template <int RPW, int MT>
-__device__ __forceinline__ void consume_275(const uint8_t* stage, int lane, const float* xs,
-                                            const float* qs, int64_t gstride_x, int64_t qstride,
-                                            float (&acc)[RPW][MT]) {
-  constexpr int CHB = 32 * 22;
-  // 22 bytes at stage + 22*lane (2-byte aligned): load 6 aligned words and
-  // realign by 0 or 2 bytes.
-  uint32_t w[RPW][6];
-#pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const uint8_t* p = stage + r * (CHB + 16) + 22 * lane;
-    const uint32_t* a4 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
-    const uint32_t sh = (reinterpret_cast<uintptr_t>(p) & 3u) * 8u;  // 0 or 16
+// 2.75: 22 bytes (21 full bytes of 3 states + tail byte: state | scale).
+// Returns the dot and the embedded scale code via *sc.
+template <class X>
+__device__ __forceinline__ float dot_275(const uint8_t* gp, const X& x, float q, uint32_t one,
+                                         float* sc) {
+  const uint32_t* a4 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(3));
+  const uint32_t sh = (reinterpret_cast<uintptr_t>(gp) & 3u) * 8u;  // 0 or 16
+  uint32_t w[6];
+  {
     uint32_t raw[7];
 #pragma unroll
     for (int i = 0; i < 7; ++i) raw[i] = a4[i];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) w[r][i] = __funnelshift_r(raw[i], raw[i + 1], sh);
+    for (int i = 0; i < 6; ++i) w[i] = __funnelshift_r(raw[i], raw[i + 1], sh);
   }
-  float2 p1[RPW][MT], p2[RPW][MT];  // p1 = (c16, c64), p2 = (c256, c256')
-#pragma unroll
-  for (int r = 0; r < RPW; ++r)
-#pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      p1[r][m] = make_float2(0.f, 0.f);
-      p2[r][m] = make_float2(0.f, 0.f);
-    }
+  float2 p1 = make_float2(0.f, 0.f), p1b = make_float2(0.f, 0.f), p2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int wi = 0; wi < 5; ++wi) {
-    float4 xv[MT][3];
-#pragma unroll
-    for (int m = 0; m < MT; ++m)
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        xv[m][k] = *reinterpret_cast<const float4*>(xs + m * gstride_x + 12 * wi + 4 * k);
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const uint32_t v = w[r][wi];
-      const uint32_t u0 = v << 15, u1 = v << 7, u2 = v >> 1, u3 = v >> 9;
-      const uint32_t u[4] = {u0, u1, u2, u3};
-      float2 f01[4];
-      float f2[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        f01[b] = make_float2(as_f((u[b] & 0x00780000u) | kOne), as_f((u[b] & 0x001E0000u) | kOne));
-        f2[b] = as_f((u[b] & 0x00078000u) | kOne);
-      }
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        p1[r][m] = __ffma2_rn(f01[0], make_float2(xv[m][0].x, xv[m][0].y), p1[r][m]);
-        p1[r][m] = __ffma2_rn(f01[1], make_float2(xv[m][0].z, xv[m][0].w), p1[r][m]);
-        p1[r][m] = __ffma2_rn(f01[2], make_float2(xv[m][1].x, xv[m][1].y), p1[r][m]);
-        p1[r][m] = __ffma2_rn(f01[3], make_float2(xv[m][1].z, xv[m][1].w), p1[r][m]);
-        p2[r][m] = __ffma2_rn(make_float2(f2[0], f2[1]), make_float2(xv[m][2].x, xv[m][2].y), p2[r][m]);
-        p2[r][m] = __ffma2_rn(make_float2(f2[2], f2[3]), make_float2(xv[m][2].z, xv[m][2].w), p2[r][m]);
-      }
-    }
+    const uint32_t v = w[wi];
+    const uint32_t u[4] = {v << 15, v << 7, v >> 1, v >> 9};
+    const float4 x0 = x.f4(3 * wi), x1 = x.f4(3 * wi + 1), x2 = x.f4(3 * wi + 2);
+    p1 = __ffma2_rn(make_float2(fm<0x00780000u>(u[0], one), fm<0x001E0000u>(u[0], one)), make_float2(x0.x, x0.y), p1);
+    p1b = __ffma2_rn(make_float2(fm<0x00780000u>(u[1], one), fm<0x001E0000u>(u[1], one)), make_float2(x0.z, x0.w), p1b);
+    p1 = __ffma2_rn(make_float2(fm<0x00780000u>(u[2], one), fm<0x001E0000u>(u[2], one)), make_float2(x1.x, x1.y), p1);
+    p1b = __ffma2_rn(make_float2(fm<0x00780000u>(u[3], one), fm<0x001E0000u>(u[3], one)), make_float2(x1.z, x1.w), p1b);
+    p2 = __ffma2_rn(make_float2(fm<0x00078000u>(u[0], one), fm<0x00078000u>(u[1], one)), make_float2(x2.x, x2.y), p2);
+    p2 = __ffma2_rn(make_float2(fm<0x00078000u>(u[2], one), fm<0x00078000u>(u[3], one)), make_float2(x2.z, x2.w), p2);
   }
-  // Word 5: byte 20 (weights 60..62) and the tail byte 21.
-  {
-    float4 xv[MT];
-#pragma unroll
-    for (int m = 0; m < MT; ++m) xv[m] = *reinterpret_cast<const float4*>(xs + m * gstride_x + 60);
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const uint32_t v = w[r][5];
-      const uint32_t u0 = v << 15;
-      const float2 f01 = make_float2(as_f((u0 & 0x00780000u) | kOne), as_f((u0 & 0x001E0000u) | kOne));
-      const float f2 = as_f((u0 & 0x00078000u) | kOne);
-      const float tail_state = float(int((v >> 12) & 0xF) - 8);
-      const float sc = float((v >> 8) & 0xF);
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        p1[r][m] = __ffma2_rn(f01, make_float2(xv[m].x, xv[m].y), p1[r][m]);
-        const float c256 = fmaf(f2, xv[m].z, p2[r][m].x + p2[r][m].y);
-        float dot = fmaf(16.f, p1[r][m].x, fmaf(64.f, p1[r][m].y, fmaf(256.f, c256, -qs[m * qstride])));
-        dot = fmaf(tail_state, xv[m].w, dot);
-        acc[r][m] = fmaf(sc, dot, acc[r][m]);
-      }
-    }
-  }
+  // word 5: byte 20 (weights 60..62) and the tail byte 21
+  const uint32_t v = w[5];
+  const uint32_t u0 = v << 15;
+  const float4 xt = x.f4(15);
+  p1 = __ffma2_rn(make_float2(fm<0x00780000u>(u0, one), fm<0x001E0000u>(u0, one)), make_float2(xt.x, xt.y), p1);
+  const float c256 = fmaf(fm<0x00078000u>(u0, one), xt.z, p2.x + p2.y);
+  float dot = fmaf(16.f, p1.x + p1b.x, fmaf(64.f, p1.y + p1b.y, fmaf(256.f, c256, -q)));
+  dot = fmaf(float(int((v >> 12) & 0xF) - 8), xt.w, dot);
+  *sc = float((v >> 8) & 0xF);
+  return dot;
 }
 
-template <int RPW, int MT>
-__device__ __forceinline__ void consume_25(const uint8_t* stage, int lane, const float* xs,
-                                           const float* qs, int64_t gstride_x, int64_t qstride,
-                                           float (&acc)[RPW][MT]) {
-  constexpr int CHB = 32 * 20;
-  uint32_t w[RPW][5];
+// 2.5: 20 bytes = 10 16-bit words (9 full + tail: state | 13-bit scale).
+template <class X>
+__device__ __forceinline__ float dot_25(const uint8_t* gp, const X& x, float q, uint32_t one,
+                                        float* sc) {
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(gp);
+  uint32_t w[5];
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const uint32_t* p = reinterpret_cast<const uint32_t*>(stage + r * (CHB + 16) + 20 * lane);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) w[r][i] = p[i];
-  }
-  // Accumulator pairs: pa = (j0,j1) (8,32); pb = (j2,j3) (128,8);
-  //                    pc = (j4,j5) (32,128); pd = (j6lo, j6hi) (512,512)
-  float2 pa[RPW][MT], pb[RPW][MT], pc[RPW][MT], pd[RPW][MT];
-#pragma unroll
-  for (int r = 0; r < RPW; ++r)
-#pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      pa[r][m] = pb[r][m] = pc[r][m] = pd[r][m] = make_float2(0.f, 0.f);
-    }
+  for (int i = 0; i < 5; ++i) w[i] = p[i];
+  float2 pa = make_float2(0.f, 0.f), pb = pa, pc = pa, pd = pa;
+  float dot = 0.f;
 #pragma unroll
   for (int u = 0; u < 5; ++u) {
-    float4 xv[MT][4];
+    const uint32_t v = w[u];
+    const uint32_t a7 = v << 7, a14 = v << 14, b9 = v >> 9, b2 = v >> 2;
+    const float4 x0 = x.f4(4 * u), x1 = x.f4(4 * u + 1), x2 = x.f4(4 * u + 2), x3 = x.f4(4 * u + 3);
+    pa = __ffma2_rn(make_float2(fm<0x00700000u>(a7, one), fm<0x001C0000u>(a7, one)), make_float2(x0.x, x0.y), pa);
+    pb = __ffma2_rn(make_float2(fm<0x00070000u>(a7, one), fm<0x00700000u>(a14, one)), make_float2(x0.z, x0.w), pb);
+    pc = __ffma2_rn(make_float2(fm<0x001C0000u>(a14, one), fm<0x00070000u>(a14, one)), make_float2(x1.x, x1.y), pc);
+    if (u < 4) {
+      pa = __ffma2_rn(make_float2(fm<0x00700000u>(b9, one), fm<0x001C0000u>(b9, one)), make_float2(x1.z, x1.w), pa);
+      pb = __ffma2_rn(make_float2(fm<0x00070000u>(b9, one), fm<0x00700000u>(b2, one)), make_float2(x2.x, x2.y), pb);
+      pc = __ffma2_rn(make_float2(fm<0x001C0000u>(b2, one), fm<0x00070000u>(b2, one)), make_float2(x2.z, x2.w), pc);
+      pd = __ffma2_rn(make_float2(fm<0x0001C000u>(a14, one), fm<0x0001C000u>(b2, one)), make_float2(x3.x, x3.y), pd);
+    } else {
+      const float d6 = fmaf(fm<0x0001C000u>(a14, one), x3.x, pd.x + pd.y);
+      dot = fmaf(8.f, pa.x + pb.y, fmaf(32.f, pa.y + pc.x, fmaf(128.f, pb.x + pc.y, fmaf(512.f, d6, -q))));
+      dot = fmaf(float(int(v >> 29) - 4), x3.z, dot);
+      *sc = float((v >> 16) & 0x1FFFu);
+    }
+  }
+  return dot;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-level reduction of N values per lane (N a power of two <= 32): after
+// the call, lane l holds the warp total of value (l >> (5 - log2 N)).
+// N - 1 + 5 - log2(N) shuffles instead of 5N.
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ float reduce_multi(float (&v)[N], int lane) {
+  float cur[N];
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
+  for (int i = 0; i < N; ++i) cur[i] = v[i];
+  int n = N;
+  int off = 16;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        xv[m][k] = *reinterpret_cast<const float4*>(xs + m * gstride_x + 16 * u + 4 * k);
+  for (int k = 0; (1 << k) < N; ++k) {
+    const int half = n / 2;
+    const bool up = lane & off;
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const uint32_t v = w[r][u];
-      // low stored word: v<<7 puts shifts 13,11,9 at 20,18,16; v<<14 puts 6,4,2,0 at 20,18,16,14
-      const uint32_t a7 = v << 7, a14 = v << 14;
-      // high stored word: v>>9 puts 29,27,25 at 20,18,16; v>>2 puts 22,20,18,16 at 20,18,16,14
-      const uint32_t b9 = v >> 9, b2 = v >> 2;
-      const float2 lo01 = make_float2(as_f((a7 & 0x00700000u) | kOne), as_f((a7 & 0x001C0000u) | kOne));
-      const float2 lo23 = make_float2(as_f((a7 & 0x00070000u) | kOne), as_f((a14 & 0x00700000u) | kOne));
-      const float2 lo45 = make_float2(as_f((a14 & 0x001C0000u) | kOne), as_f((a14 & 0x00070000u) | kOne));
-      const float2 hi01 = make_float2(as_f((b9 & 0x00700000u) | kOne), as_f((b9 & 0x001C0000u) | kOne));
-      const float2 hi23 = make_float2(as_f((b9 & 0x00070000u) | kOne), as_f((b2 & 0x00700000u) | kOne));
-      const float2 hi45 = make_float2(as_f((b2 & 0x001C0000u) | kOne), as_f((b2 & 0x00070000u) | kOne));
-      const float2 j6 = make_float2(as_f((a14 & 0x0001C000u) | kOne), as_f((b2 & 0x0001C000u) | kOne));
-      if (u < 4) {
+    for (int j = 0; j < N / 2; ++j) {
+      if (j < half) {
+        const float send = up ? cur[j] : cur[j + half];
+        const float keep = up ? cur[j + half] : cur[j];
+        cur[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    n = half;
+    off >>= 1;
+  }
+  float t = cur[0];
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          pa[r][m] = __ffma2_rn(lo01, make_float2(xv[m][0].x, xv[m][0].y), pa[r][m]);
-          pb[r][m] = __ffma2_rn(lo23, make_float2(xv[m][0].z, xv[m][0].w), pb[r][m]);
-          pc[r][m] = __ffma2_rn(lo45, make_float2(xv[m][1].x, xv[m][1].y), pc[r][m]);
-          pa[r][m] = __ffma2_rn(hi01, make_float2(xv[m][1].z, xv[m][1].w), pa[r][m]);
-          pb[r][m] = __ffma2_rn(hi23, make_float2(xv[m][2].x, xv[m][2].y), pb[r][m]);
-          pc[r][m] = __ffma2_rn(hi45, make_float2(xv[m][2].z, xv[m][2].w), pc[r][m]);
-          pd[r][m] = __ffma2_rn(j6, make_float2(xv[m][3].x, xv[m][3].y), pd[r][m]);
-        }
-      } else {
-        // stored word 8 (full, low half) + tail word 9 (high half).
-        const float tail_state = float(int(v >> 29) - 4);
-        const float sc = float((v >> 16) & 0x1FFFu);
+  for (; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  return t;
+}
+
+template <int XDT>
+__device__ __forceinline__ void load_x64(const void* x, int64_t base, float (&out)[64]) {
+  constexpr int dtype = XDT;
+  if constexpr (dtype == CCQ_DTYPE_F32) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(x) + base);
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          pa[r][m] = __ffma2_rn(lo01, make_float2(xv[m][0].x, xv[m][0].y), pa[r][m]);
-          pb[r][m] = __ffma2_rn(lo23, make_float2(xv[m][0].z, xv[m][0].w), pb[r][m]);
-          pc[r][m] = __ffma2_rn(lo45, make_float2(xv[m][1].x, xv[m][1].y), pc[r][m]);
-          const float d6 = fmaf(j6.x, xv[m][3].x, pd[r][m].x + pd[r][m].y);
-          float dot = fmaf(8.f, pa[r][m].x + pb[r][m].y,
-                           fmaf(32.f, pa[r][m].y + pc[r][m].x,
-                                fmaf(128.f, pb[r][m].x + pc[r][m].y, fmaf(512.f, d6, -qs[m * qstride]))));
-          dot = fmaf(tail_state, xv[m][3].z, dot);
-          acc[r][m] = fmaf(sc, dot, acc[r][m]);
+    for (int i = 0; i < 16; ++i) {
+      const float4 v = __ldg(p + i);
+      out[4 * i] = v.x;
+      out[4 * i + 1] = v.y;
+      out[4 * i + 2] = v.z;
+      out[4 * i + 3] = v.w;
+    }
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + base);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = __ldg(p + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (dtype == CCQ_DTYPE_BF16) {
+          out[8 * i + 2 * j] = __uint_as_float(w[j] << 16);
+          out[8 * i + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        } else {
+          out[8 * i + 2 * j] = __half2float(__ushort_as_half(uint16_t(w[j] & 0xFFFF)));
+          out[8 * i + 2 * j + 1] = __half2float(__ushort_as_half(uint16_t(w[j] >> 16)));
         }
       }
     }
@@ -361,31 +343,43 @@ __device__ __forceinline__ void consume_25(const uint8_t* stage, int lane, const
 
 // ---------------------------------------------------------------------------
 // The streaming kernel.
-// Shared memory: [x: MT][gpr][XG] f32 | [Q: MT][gpr] f32 | per-warp rings:
-//   stages x RPW x (CHB + 16 nibble bytes) | mbarriers
+// Shared memory: [partials: rows_per_cta_max][nch][MT] f32
+//                [x (M > 1 only): MT][gpr][XG] f32
+//                [rings: warps][S][SB] | [mbarriers: warps][S]
+// One stage SB = RPW * (CGB codes + 16 nibble bytes + 16 plan bytes).
 // ---------------------------------------------------------------------------
-template <int FAM, int RPW, int MT>
+template <int FAM, int RPW, int MT, int S, int XDT>
 __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   using T = G64<FAM>;
-  constexpr int CHB = 32 * T::PB;
-  constexpr int RB = CHB + 16;  // ring bytes per row per stage
+  constexpr bool XREG = MT == 1;
+  constexpr bool SIDE = FAM == kF206;
+  constexpr int CGB = (32 * T::PB + 15) & ~15;
+  constexpr int SB = RPW * (CGB + (SIDE ? 32 : 0));
   extern __shared__ __align__(128) uint8_t smem[];
+  const DevLayout& L = a.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int64_t gpr = a.gpr;
-  float* xs = reinterpret_cast<float*>(smem);
-  const int64_t xstride = gpr * T::XG;  // floats per token
-  float* qs = xs + MT * xstride;
-  uint8_t* rings = reinterpret_cast<uint8_t*>(qs + ((MT * gpr + 31) / 32) * 32);
-  const int S = a.stages;
-  uint8_t* ring = rings + size_t(warp) * S * RPW * RB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rings + size_t(nwarps) * S * RPW * RB) + warp * S;
+  const int nch = L.nch;
+  const int c = warp % nch, stream = warp / nch;
+  const int64_t rows = L.rows, gpr = L.gpr;
+  const int64_t r_begin = int64_t(blockIdx.x) * rows / gridDim.x;
+  const int64_t r_end = int64_t(blockIdx.x + 1) * rows / gridDim.x;
+  const int nrows = int(r_end - r_begin);
+  // rows of this stream: contiguous
+  const int64_t s_begin = r_begin + int64_t(stream) * nrows / a.streams;
+  const int64_t s_end = r_begin + int64_t(stream + 1) * nrows / a.streams;
+  const int ntiles = int((s_end - s_begin + RPW - 1) / RPW);
 
-  // Work: whole row tiles, round-robin over all warps of the grid.
-  const int64_t gw = int64_t(blockIdx.x) * nwarps + warp;
-  const int64_t W = int64_t(gridDim.x) * nwarps;
-  const int nch = a.nchunks;
-  const int64_t my_tiles = gw < a.tiles ? (a.tiles - gw + W - 1) / W : 0;
-  const int64_t n_items = my_tiles * nch;
+  float* part = reinterpret_cast<float*>(smem);
+  float* xs = part + ((a.rows_per_cta_max * nch * MT + 31) & ~31);
+  const int64_t xstride = XREG ? 0 : gpr * T::XG;
+  uint8_t* rings = reinterpret_cast<uint8_t*>(xs + MT * xstride);
+  uint8_t* ring = rings + size_t(warp) * S * SB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rings + size_t(nwarps) * S * SB) + warp * S;
+
+  const int g0 = c * kChunk;
+  const int ng = int(gpr - g0 < kChunk ? gpr - g0 : kChunk);
+  const uint8_t* src_codes = L.codes + (uint64_t(c) * rows) * CGB;
+  const uint8_t* src_nib = SIDE ? L.nibbles + (uint64_t(c) * rows) * 16 : nullptr;
 
   if (lane == 0)
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -393,128 +387,140 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   __syncwarp();
 
   const uint64_t pol = policy_evict_first();
-  auto issue = [&](int64_t item) {
-    const int s = int(item % S);
-    const int64_t tile = gw + (item / nch) * W;
-    const int c = int(item % nch);
-    const int g0 = c * 32;
-    const int ng = int((gpr - g0 < 32 ? gpr - g0 : 32));
-    const uint32_t cb = uint32_t((ng * T::PB + 15) & ~15);
-    const uint32_t nb = uint32_t(((ng + 1) / 2 + 15) & ~15);
-    const int64_t r0 = tile * RPW;
-    const int nr = int((a.rows - r0 < RPW ? a.rows - r0 : int64_t(RPW)));
-    const bool side = FAM == kF206;
+  auto issue = [&](int t) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bars[s], uint32_t(nr) * (cb + (side ? nb : 0u)));
-      for (int r = 0; r < nr; ++r) {
-        uint8_t* dst = ring + (size_t(s) * RPW + r) * RB;
-        bulk_g2s_evict_first(dst, a.codes + (r0 + r) * a.code_stride + int64_t(g0) * T::PB, cb,
-                             &bars[s], pol);
-        if (side)
-          bulk_g2s_evict_first(dst + CHB, a.nibbles + (r0 + r) * a.nib_stride + g0 / 2, nb,
-                               &bars[s], pol);
+      const int s = t % S;
+      const int64_t r0 = s_begin + int64_t(t) * RPW;
+      const uint32_t nr = uint32_t(s_end - r0 < RPW ? s_end - r0 : RPW);
+      uint8_t* dst = ring + s * SB;
+      mbar_arrive_expect_tx(&bars[s], nr * (CGB + (SIDE ? 32u : 0u)));
+      bulk_g2s_evict_first(dst, src_codes + r0 * CGB, nr * CGB, &bars[s], pol);
+      if constexpr (SIDE) {
+        bulk_g2s_evict_first(dst + RPW * CGB, src_nib + r0 * 16, nr * 16, &bars[s], pol);
+        bulk_g2s(dst + RPW * (CGB + 16), L.plan + r0, nr * 16, &bars[s]);
       }
     }
   };
+#pragma unroll
+  for (int t = 0; t < S; ++t)
+    if (t < ntiles) issue(t);
 
-  // Prefetch the first stages while x is being staged.
-  const int64_t pre = (n_items < S ? n_items : int64_t(S));
-  for (int64_t i = 0; i < pre; ++i) issue(i);
-
-  // Stage x (f32, permuted per family) and the per-group correction Q.
-  for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr * 64; e += blockDim.x) {
-    const int m = int(e / (gpr * 64));
-    const int64_t k = e - int64_t(m) * gpr * 64;
-    const int64_t g = k >> 6;
-    const int i = int(k & 63);
-    const float v = m < a.M ? load_x(a.x, a.x_dtype, int64_t(m) * a.x_stride + k) : 0.f;
-    xs[m * xstride + g * T::XG + T::perm(i)] = v;
-  }
-  __syncthreads();
-  for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr; e += blockDim.x) {
-    const int m = int(e / gpr);
-    const int64_t g = e - int64_t(m) * gpr;
-    const float* xg = xs + m * xstride + g * T::XG;
+  // Activations: registers (M = 1) or shared memory (M > 1), and Q.
+  const int g = g0 + lane;
+  const bool active = lane < ng;
+  XGroup<FAM, XREG> xg;
+  float qv[MT];
+  if constexpr (XREG) {
+    float xv[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) xv[i] = 0.f;
+    if (active && a.M > 0) load_x64<XDT>(a.x, int64_t(g) * 64, xv);
     float q = 0.f;
-    for (int i = 0; i < 64; ++i)
-      if (!T::exact_tail(i)) q = fmaf(T::cls(i) + float(T::ZP), xg[T::perm(i)], q);
-    qs[m * gpr + g] = q;
+    float xp[T::XG];
+#pragma unroll
+    for (int i = 0; i < T::XG; ++i) xp[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      xp[T::perm(i)] = xv[i];
+      if (!T::exact_tail(i)) q = fmaf(T::cls(i) + float(T::ZP), xv[i], q);
+    }
+#pragma unroll
+    for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(xp[4 * k], xp[4 * k + 1], xp[4 * k + 2], xp[4 * k + 3]);
+    qv[0] = q;
+  } else {
+    for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr * 64; e += blockDim.x) {
+      const int m = int(e / (gpr * 64));
+      const int64_t k = e - int64_t(m) * gpr * 64;
+      const float v = m < a.M ? load_x(a.x, a.x_dtype, int64_t(m) * a.x_stride + k) : 0.f;
+      xs[m * xstride + (k >> 6) * T::XG + T::perm(int(k & 63))] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      float q = 0.f;
+      if (active) {
+        const float* xq = xs + m * xstride + int64_t(g) * T::XG;
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (!T::exact_tail(i)) q = fmaf(T::cls(i) + float(T::ZP), xq[T::perm(i)], q);
+      }
+      qv[m] = q;
+    }
   }
-  __syncthreads();
+  uint32_t one;
+  asm volatile("mov.b32 %0, 0x3f800000;" : "=r"(one));
 
-  float acc[RPW][MT];
-  WidenPlan pl[RPW];
-  uint32_t sel[RPW][4];
-  float scf[RPW];
-  int64_t cur_tile = -1;
-  for (int64_t it = 0; it < n_items; ++it) {
-    const int s = int(it % S);
-    const int64_t tile = gw + (it / nch) * W;
-    const int c = int(it % nch);
-    const int64_t r0 = tile * RPW;
-    if (tile != cur_tile) {
-      cur_tile = tile;
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t % S;
+    const int64_t r0 = s_begin + int64_t(t) * RPW;
+    float acc[RPW * MT];
+#pragma unroll
+    for (int i = 0; i < RPW * MT; ++i) acc[i] = 0.f;
+    mbar_wait(&bars[s], uint32_t((t / S) & 1));
+    const uint8_t* st = ring + s * SB;
+    if (active) {
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-#pragma unroll
-        for (int m = 0; m < MT; ++m) acc[r][m] = 0.f;
-        if constexpr (FAM == kF206) {
-          const int64_t row = (r0 + r < a.rows ? r0 + r : a.rows - 1);
-          pl[r] = a.plan[row];
-          // byte b of a word -> byte position sh/8 of q (zeros elsewhere)
-          const uint32_t pos = pl[r].sh >> 3;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) sel[r][b] = (0x4444u & ~(0xFu << (4 * pos))) | (uint32_t(b) << (4 * pos));
+        const uint8_t* gp = st + r * CGB + lane * T::PB;
+        WidenPlan pl;
+        uint32_t sel[4];
+        float sc206 = 0.f;
+        if constexpr (SIDE) {
+          const uint4 pv = lds128(st + RPW * (CGB + 16) + r * 16);
+          pl.C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
+          pl.M = pv.z;
+          pl.sel = pv.w;
+          const uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
+          sel[0] = base;
+          sel[1] = base + step;
+          sel[2] = base + 2 * step;
+          sel[3] = base + 3 * step;
+          const uint8_t nib = st[RPW * CGB + r * 16 + (lane >> 1)];
+          sc206 = float((nib >> (4 * (lane & 1))) & 0xF);
         }
-      }
-    }
-    mbar_wait(&bars[s], uint32_t((it / S) & 1));
-    const int g = c * 32 + lane;
-    if (g < gpr) {
-      const uint8_t* st = ring + size_t(s) * RPW * RB;
-      const float* xg = xs + g * T::XG;
-      const float* qg = qs + g;
-      if constexpr (FAM == kF206) {
 #pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const uint8_t nib = st[r * RB + CHB + (lane >> 1)];
-          scf[r] = float((nib >> (4 * (lane & 1))) & 0xF);
+        for (int m = 0; m < MT; ++m) {
+          XGroup<FAM, XREG> xm = xg;
+          if constexpr (!XREG) xm.p = xs + m * xstride + int64_t(g) * T::XG;
+          float sc, dot;
+          if constexpr (FAM == kF206) {
+            dot = dot_206(gp, xm, qv[m], pl, sel, one);
+            sc = sc206;
+          } else if constexpr (FAM == kF275) {
+            dot = dot_275(gp, xm, qv[m], one, &sc);
+          } else {
+            dot = dot_25(gp, xm, qv[m], one, &sc);
+          }
+          acc[r * MT + m] = sc * dot;
         }
-        consume_206<RPW, MT>(st, lane, xg, qg, xstride, gpr, pl, sel, scf, acc);
-      } else if constexpr (FAM == kF275) {
-        consume_275<RPW, MT>(st, lane, xg, qg, xstride, gpr, acc);
-      } else {
-        consume_25<RPW, MT>(st, lane, xg, qg, xstride, gpr, acc);
       }
     }
     __syncwarp();
     fence_proxy_async_smem();
-    if (it + S < n_items) issue(it + S);
+    if (t + S < ntiles) issue(t + S);
 
-    if (c == nch - 1) {
-      // Tile done: reduce across lanes, scale by the row super scale, store.
-#pragma unroll
-      for (int r = 0; r < RPW; ++r)
-#pragma unroll
-        for (int m = 0; m < MT; ++m) acc[r][m] = warp_sum(acc[r][m]);
-      if (lane < RPW * MT) {
-        const int r = lane / MT, m = lane % MT;
-        const int64_t row = r0 + r;
-        float v = 0.f;
-#pragma unroll
-        for (int rr = 0; rr < RPW; ++rr)
-#pragma unroll
-          for (int mm = 0; mm < MT; ++mm)
-            if (rr == r && mm == m) v = acc[rr][mm];
-        if (row < a.rows && m < a.M) {
-          v *= a.super[row];
-          if (a.y_dtype == CCQ_DTYPE_F32)
-            static_cast<float*>(a.y)[int64_t(m) * a.y_stride + row] = v;
-          else
-            static_cast<__nv_bfloat16*>(a.y)[int64_t(m) * a.y_stride + row] = __float2bfloat16_rn(v);
-        }
-      }
+    // Chunk partial of each (row, token): one multi-value warp reduction.
+    const float v = reduce_multi<RPW * MT>(acc, lane);
+    constexpr int SPAN = 32 / (RPW * MT);
+    if ((lane & (SPAN - 1)) == 0) {
+      const int idx = lane / SPAN;
+      const int r = idx / MT, m = idx % MT;
+      if (r0 + r < s_end) part[(int(r0 + r - r_begin) * nch + c) * MT + m] = v;
     }
+  }
+  __syncthreads();
+  // Sum chunk partials in a fixed order; scale by the row super scale.
+  for (int e = threadIdx.x; e < nrows * MT; e += blockDim.x) {
+    const int rl = e / MT, m = e % MT;
+    if (m >= a.M) continue;
+    float v = 0.f;
+    for (int cc = 0; cc < nch; ++cc) v += part[(rl * nch + cc) * MT + m];
+    const int64_t row = r_begin + rl;
+    v *= L.super[row];
+    if (a.y_dtype == CCQ_DTYPE_F32)
+      static_cast<float*>(a.y)[int64_t(m) * a.y_stride + row] = v;
+    else
+      static_cast<__nv_bfloat16*>(a.y)[int64_t(m) * a.y_stride + row] = __float2bfloat16_rn(v);
   }
 }
 
@@ -523,16 +529,11 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
 // lanes stride over groups, exact per-weight decode (kernels.cpp:60-93).
 // ---------------------------------------------------------------------------
 struct GenericArgs {
-  const uint8_t* codes;
-  const uint8_t* nibbles;
-  const float* super;
-  const WidenPlan* plan;
+  DevLayout L;
   const void* x;
   void* y;
   int x_dtype, y_dtype;
-  int64_t rows, cols, gpr, M;
-  uint64_t code_stride, nib_stride;
-  Geometry geo;
+  int64_t M;
 };
 
 template <int FAM>
@@ -540,36 +541,37 @@ __global__ void __launch_bounds__(256) gemv_generic(GenericArgs a) {
   constexpr FamilyConst fc = family_const(FAM);
   constexpr int TM = 8;
   const int lane = threadIdx.x & 31;
+  const DevLayout& L = a.L;
   const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (row >= a.rows) return;
+  if (row >= L.rows) return;
   WidenPlan pl{};
-  if constexpr (fc.cluster) pl = a.plan[row];
-  const float sup = a.super[row];
+  if constexpr (fc.cluster) pl = L.plan[row];
+  const float sup = L.super[row];
   for (int64_t m0 = 0; m0 < a.M; m0 += TM) {
     float acc[TM];
 #pragma unroll
     for (int t = 0; t < TM; ++t) acc[t] = 0.f;
-    for (int64_t gj = lane; gj < a.gpr; gj += 32) {
-      const uint8_t* p = a.codes + row * a.code_stride + gj * a.geo.payload_bytes;
+    for (int64_t gj = lane; gj < L.gpr; gj += 32) {
+      const uint8_t* p = L.group(row, gj);
       auto word = [&](int w) -> uint32_t {
         const uint8_t* q = p + w * fc.word_bytes;
         return fc.word_bytes == 2 ? (uint32_t(q[0]) | (uint32_t(q[1]) << 8)) : uint32_t(q[0]);
       };
       uint32_t sc;
-      if (a.geo.embedded_scale) sc = word(a.geo.full_words) & fc.scale_mask;
-      else sc = (a.nibbles[row * a.nib_stride + gj / 2] >> (4 * (gj & 1))) & 0xF;
+      if (L.geo.embedded_scale) sc = word(L.geo.full_words) & fc.scale_mask;
+      else sc = L.nibble(row, gj);
       const float scale = __fmul_rn(float(sc), sup);
       int idx = 0;
-      for (int w = 0; w < a.geo.words_per_group; ++w) {
+      for (int w = 0; w < L.geo.words_per_group; ++w) {
         uint32_t code = word(w);
         if constexpr (fc.cluster) code = widen_hi(code, pl) >> 8;
-        const int nk = w < a.geo.full_words ? fc.wpw : 1;
+        const int nk = w < L.geo.full_words ? fc.wpw : 1;
         for (int k = 0; k < nk; ++k, ++idx) {
           const float wv = __fmul_rn(float(int((code >> fc.shifts[k]) & fc.weight_mask) - fc.zero_point), scale);
-          const int64_t col = gj * a.geo.group_size + idx;
+          const int64_t col = gj * L.geo.group_size + idx;
 #pragma unroll
           for (int t = 0; t < TM; ++t)
-            if (m0 + t < a.M) acc[t] = fmaf(wv, load_x(a.x, a.x_dtype, (m0 + t) * a.cols + col), acc[t]);
+            if (m0 + t < a.M) acc[t] = fmaf(wv, load_x(a.x, a.x_dtype, (m0 + t) * L.cols + col), acc[t]);
         }
       }
     }
@@ -577,12 +579,13 @@ __global__ void __launch_bounds__(256) gemv_generic(GenericArgs a) {
     for (int t = 0; t < TM; ++t) {
       const float v = warp_sum(acc[t]);
       if (lane == 0 && m0 + t < a.M) {
-        if (a.y_dtype == CCQ_DTYPE_F32) static_cast<float*>(a.y)[(m0 + t) * a.rows + row] = v;
-        else static_cast<__nv_bfloat16*>(a.y)[(m0 + t) * a.rows + row] = __float2bfloat16_rn(v);
+        if (a.y_dtype == CCQ_DTYPE_F32) static_cast<float*>(a.y)[(m0 + t) * L.rows + row] = v;
+        else static_cast<__nv_bfloat16*>(a.y)[(m0 + t) * L.rows + row] = __float2bfloat16_rn(v);
       }
     }
   }
 }
+
 
 int num_sms(int device) {
   static int cached[64] = {0};
@@ -595,92 +598,76 @@ int num_sms(int device) {
   return cached[device];
 }
 
-template <int FAM, int RPW, int MT>
-int launch_stream(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
+template <int FAM, int RPW, int MT, int S, int XDT>
+int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
                   void* y, int y_dtype, cudaStream_t s) {
   using T = G64<FAM>;
-  constexpr int RB = 32 * T::PB + 16;
+  constexpr int CGB = (32 * T::PB + 15) & ~15;
+  constexpr int SB = RPW * (CGB + (FAM == kF206 ? 32 : 0));
   GemvArgs a{};
-  a.codes = m->codes;
-  a.nibbles = m->nibbles;
-  a.super = m->super;
-  a.plan = m->plan;
+  a.L = layout_of(m);
   const size_t xb = x_dtype == CCQ_DTYPE_F32 ? 4 : 2;
   const size_t yb = y_dtype == CCQ_DTYPE_F32 ? 4 : 2;
   a.x = static_cast<const uint8_t*>(x) + size_t(M0) * size_t(m->cols) * xb;
   a.y = static_cast<uint8_t*>(y) + size_t(M0) * size_t(m->rows) * yb;
   a.x_dtype = x_dtype;
   a.y_dtype = y_dtype;
-  a.rows = m->rows;
-  a.cols = m->cols;
-  a.gpr = m->gpr;
-  a.code_stride = m->code_stride;
-  a.nib_stride = m->nib_stride;
   a.M = int(Mn);
   a.x_stride = m->cols;
   a.y_stride = m->rows;
-  a.tiles = (m->rows + RPW - 1) / RPW;
-  a.nchunks = int((m->gpr + 31) / 32);
 
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = num_sms(dev);
-  const size_t xbytes = size_t(MT) * m->gpr * T::XG * 4 + size_t((MT * m->gpr + 31) / 32) * 32 * 4;
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // Warps per CTA: enough tiles for every warp, balanced across the grid.
-  int best_w = 4;
-  double best_eff = -1;
-  for (int w = 16; w >= 4; --w) {
-    const double W = double(sms) * w;
-    const double per = double(a.tiles) / W;
-    const double eff = per / std::ceil(per) * std::min(1.0, per * 4.0);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best_w = w;
-    }
-  }
-  int stages = 4;
-  size_t smem = 0;
-  for (;; --stages) {
-    smem = xbytes + size_t(best_w) * stages * RPW * RB + size_t(best_w) * stages * 8 + 128;
-    if (smem <= size_t(max_smem) || stages == 2) break;
-  }
-  while (smem > size_t(max_smem) && best_w > 2) {
-    --best_w;
-    smem = xbytes + size_t(best_w) * stages * RPW * RB + size_t(best_w) * stages * 8 + 128;
-  }
-  if (smem > size_t(max_smem)) return fail(CCQ_ERR_CONFIG, "activations too large for the streaming GEMV");
-  a.stages = stages;
-  auto kern = gemv_stream<FAM, RPW, MT>;
-  static thread_local size_t configured[3][5][5] = {};
-  size_t& conf = configured[FAM][RPW][MT];
+  const int64_t grid = std::min<int64_t>(sms, m->rows);
+  a.rows_per_cta_max = int((m->rows + grid - 1) / grid);
+  a.streams = std::max(1, 16 / m->nch);
+  const int warps = m->nch * a.streams;
+  const size_t xbytes = MT == 1 ? 0 : size_t(MT) * m->gpr * T::XG * 4;
+  const size_t pbytes = size_t((a.rows_per_cta_max * m->nch * MT + 31) & ~31) * 4;
+  const size_t smem = pbytes + xbytes + size_t(warps) * S * SB + size_t(warps) * S * 8 + 128;
+  if (smem > size_t(max_smem)) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");
+  auto kern = gemv_stream<FAM, RPW, MT, S, XDT>;
+  static size_t configured[3][5][5][3] = {};
+  size_t& conf = configured[FAM][RPW][MT][XDT];
   if (conf < smem) {
     CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     conf = smem;
   }
-  const int64_t warps_needed = a.tiles;
-  const int64_t grid = std::min<int64_t>(sms, (warps_needed + best_w - 1) / best_w);
-  kern<<<unsigned(grid), unsigned(best_w * 32), smem, s>>>(a);
+  kern<<<unsigned(grid), unsigned(warps * 32), smem, s>>>(a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemv launch");
 }
 
+template <int FAM, int RPW, int MT, int S>
+int launch_stream(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
+                  void* y, int y_dtype, cudaStream_t s) {
+  switch (x_dtype) {
+    case CCQ_DTYPE_F32: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_F32>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
+    case CCQ_DTYPE_BF16: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_BF16>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
+    default: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_F16>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
+  }
+}
+
 template <int FAM>
 int launch_fam(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                cudaStream_t s) {
+  using T = G64<FAM>;
+  const int64_t xk = m->gpr * T::XG * 4;  // smem bytes per staged token
   for (int64_t m0 = 0; m0 < M;) {
     const int64_t left = M - m0;
     int st;
-    if (left >= 4 && m->gpr * 64 * 4 * 4 <= 160 * 1024) {
-      st = launch_stream<FAM, 2, 4>(m, x, x_dtype, m0, 4, y, y_dtype, s);
+    if (left >= 4 && xk * 4 <= 96 * 1024) {
+      st = launch_stream<FAM, 2, 4, 2>(m, x, x_dtype, m0, 4, y, y_dtype, s);
       m0 += 4;
-    } else if (left >= 2 && m->gpr * 64 * 2 * 4 <= 160 * 1024) {
-      st = launch_stream<FAM, 4, 2>(m, x, x_dtype, m0, 2, y, y_dtype, s);
+    } else if (left >= 2 && xk * 2 <= 120 * 1024) {
+      st = launch_stream<FAM, 2, 2, 2>(m, x, x_dtype, m0, 2, y, y_dtype, s);
       m0 += 2;
     } else {
-      st = launch_stream<FAM, 4, 1>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      st = launch_stream<FAM, 4, 1, 4>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       m0 += 1;
     }
     if (st != CCQ_OK) return st;
@@ -691,8 +678,7 @@ int launch_fam(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
 template <int FAM>
 int launch_generic(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                    int y_dtype, cudaStream_t s) {
-  GenericArgs a{m->codes, m->nibbles, m->super, m->plan, x, y, x_dtype, y_dtype,
-                m->rows, m->cols, m->gpr, M, m->code_stride, m->nib_stride, m->geo};
+  GenericArgs a{layout_of(m), x, y, x_dtype, y_dtype, M};
   gemv_generic<FAM><<<unsigned((m->rows + 7) / 8), 256, 0, s>>>(a);
   count_launch();
   cudaError_t e = cudaGetLastError();
@@ -702,12 +688,12 @@ int launch_generic(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
 }  // namespace
 
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
-  return m->geo.group_size == 64 && M <= 8 && m->gpr * 64 * 4 <= 100 * 1024;
+  return m->geo.group_size == 64 && M <= 8 && m->nch <= 16;
 }
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
-  const bool fast = m->geo.group_size == 64 && m->gpr * 64 * 4 <= 100 * 1024;
+  const bool fast = m->geo.group_size == 64 && m->nch <= 16;
   switch (m->family) {
     case kF275:
       return fast ? launch_fam<kF275>(m, x, x_dtype, M, y, y_dtype, s)

@@ -6,6 +6,7 @@
 //   clustered_code_value              coding.hpp:142-150
 //   dequantize / gemv / gemv_batch    kernels.cpp:103-187 (signatures kernels.hpp:36-43)
 //   model_payload_bytes               kernels.cpp:203-207
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -75,7 +76,7 @@ bool build_widen_plan(float alpha, float beta, WidenPlan* out, bool invalid[256]
     bool all_invalid = true;
     for (int q = 0; q < 256; ++q) all_invalid &= invalid[q];
     if (all_invalid) {
-      *out = WidenPlan{0, 0, 0};
+      *out = WidenPlan{0, 0, plan_sel(0)};
       return true;
     }
     return false;
@@ -84,8 +85,8 @@ bool build_widen_plan(float alpha, float beta, WidenPlan* out, bool invalid[256]
   // exact below 2^53 and a no-op above.
   const int64_t C0 = int64_t(std::floor(std::ldexp(double(beta), 40))) + (int64_t(1) << 39);
 
-  auto verify = [&](uint32_t M, uint32_t sh, int64_t C) {
-    WidenPlan p{uint64_t(C), M, sh};
+  auto verify = [&](uint32_t M, uint32_t pos, int64_t C) {
+    WidenPlan p{uint64_t(C), M, plan_sel(pos)};
     for (int q = 0; q < 256; ++q) {
       if (invalid[q]) continue;
       const uint32_t hi = widen_hi(uint32_t(q), p);
@@ -95,23 +96,23 @@ bool build_widen_plan(float alpha, float beta, WidenPlan* out, bool invalid[256]
     return true;
   };
 
-  // Exact M: alpha * 2^(40 - sh) integral and below 2^32.
-  std::vector<std::pair<uint32_t, uint32_t>> cands;  // (M, sh)
-  for (uint32_t sh : {16u, 8u, 24u, 0u}) {
-    const double Md = std::ldexp(double(alpha), 40 - int(sh));
-    if (Md >= 0.0 && Md < 4294967296.0 && Md == std::floor(Md)) cands.push_back({uint32_t(Md), sh});
+  // Exact M: alpha * 2^(40 - 8*pos) integral and below 2^32.
+  std::vector<std::pair<uint32_t, uint32_t>> cands;  // (M, pos)
+  for (uint32_t pos : {2u, 1u, 3u, 0u}) {
+    const double Md = std::ldexp(double(alpha), 40 - 8 * int(pos));
+    if (Md >= 0.0 && Md < 4294967296.0 && Md == std::floor(Md)) cands.push_back({uint32_t(Md), pos});
   }
   // Approximate M (tiny or huge alpha): rounded, still verified exhaustively.
-  for (uint32_t sh : {0u, 8u, 16u, 24u}) {
-    const double Md = std::ldexp(double(alpha), 40 - int(sh));
-    if (Md >= 0.0 && Md < 4294967295.5) cands.push_back({uint32_t(std::llround(Md)), sh});
+  for (uint32_t pos : {0u, 1u, 2u, 3u}) {
+    const double Md = std::ldexp(double(alpha), 40 - 8 * int(pos));
+    if (Md >= 0.0 && Md < 4294967295.5) cands.push_back({uint32_t(std::llround(Md)), pos});
   }
   static const int64_t nudges[] = {0,       1,        -1,        256,        -256,
                                    65536,   -65536,   1 << 24,   -(1 << 24), int64_t(1) << 30,
                                    -(int64_t(1) << 30), int64_t(1) << 34, -(int64_t(1) << 34)};
-  for (const auto& [M, sh] : cands)
+  for (const auto& [M, pos] : cands)
     for (int64_t d : nudges)
-      if (verify(M, sh, C0 + d)) return true;
+      if (verify(M, pos, C0 + d)) return true;
   return false;
 }
 
@@ -196,34 +197,39 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   m->gpr = gpr;
   const int64_t rows = m->rows;
   const uint64_t row_bytes = uint64_t(gpr) * geo.payload_bytes;
-  m->code_stride = align_up(row_bytes ? row_bytes : 16, 16);
-  m->nib_stride = geo.embedded_scale ? 0 : align_up(size_t((gpr + 1) / 2) ? size_t((gpr + 1) / 2) : 16, 16);
+  m->nch = int((gpr + kChunk - 1) / kChunk);
+  m->cgb = uint32_t(align_up(size_t(kChunk) * geo.payload_bytes, 16));
   m->payload_bytes = uint64_t(rows) * row_bytes +
                      (geo.embedded_scale ? 0 : (uint64_t(rows) * gpr + 1) / 2) + uint64_t(rows) * 4 +
                      (fc.cluster ? uint64_t(rows) * 8 : 0);
 
-  // Host staging in the device layout.
+  // Host staging in the chunk-major device layout (ccq_internal.hpp).
+  const size_t n_cr = size_t(m->nch) * size_t(rows);  // (chunk, row) slots
   const size_t off_codes = 0;
-  const size_t off_nib = align_up(off_codes + size_t(rows) * m->code_stride, 256);
-  const size_t off_super = align_up(off_nib + size_t(rows) * m->nib_stride, 256);
+  const size_t off_nib = align_up(off_codes + n_cr * m->cgb, 256);
+  const size_t off_super = align_up(off_nib + (geo.embedded_scale ? 0 : n_cr * 16), 256);
   const size_t off_plan = align_up(off_super + size_t(rows) * 4, 256);
   const size_t total = align_up(off_plan + (fc.cluster ? size_t(rows) * sizeof(WidenPlan) : 0), 256) + 256;
   std::vector<uint8_t> host(total, 0);
   for (int64_t r = 0; r < rows; ++r) {
     const int64_t src = r0 + r;
-    if (row_bytes)
-      std::memcpy(&host[off_codes + size_t(r) * m->code_stride],
-                  v->code_payload + uint64_t(src) * row_bytes, row_bytes);
-    if (!geo.embedded_scale) {
-      uint8_t* dst = &host[off_nib + size_t(r) * m->nib_stride];
-      for (int64_t gj = 0; gj < gpr; ++gj) {
-        const uint64_t gi = uint64_t(src) * gpr + gj;
-        const uint8_t nib = (v->scale_payload[gi / 2] >> (4 * (gi % 2))) & 0xF;
-        dst[gj / 2] |= uint8_t(nib << (4 * (gj % 2)));
+    for (int c = 0; c < m->nch; ++c) {
+      const int64_t g0 = int64_t(c) * kChunk;
+      const int64_t ng = std::min<int64_t>(kChunk, gpr - g0);
+      std::memcpy(&host[off_codes + (size_t(c) * rows + r) * m->cgb],
+                  v->code_payload + uint64_t(src) * row_bytes + uint64_t(g0) * geo.payload_bytes,
+                  size_t(ng) * geo.payload_bytes);
+      if (!geo.embedded_scale) {
+        uint8_t* dst = &host[off_nib + (size_t(c) * rows + r) * 16];
+        for (int64_t j = 0; j < ng; ++j) {
+          const uint64_t gi = uint64_t(src) * gpr + g0 + j;
+          const uint8_t nib = (v->scale_payload[gi / 2] >> (4 * (gi % 2))) & 0xF;
+          dst[j / 2] |= uint8_t(nib << (4 * (j % 2)));
+        }
       }
     }
   }
-  std::memcpy(&host[off_super], v->super_scales + r0, size_t(rows) * 4);
+  if (rows) std::memcpy(&host[off_super], v->super_scales + r0, size_t(rows) * 4);
   if (fc.cluster) {
     auto* plans = reinterpret_cast<WidenPlan*>(&host[off_plan]);
     for (int64_t r = 0; r < rows; ++r) {
@@ -236,6 +242,8 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
                                         ": cluster parameters have no exact fixed-point "
                                         "widening plan");
       }
+      // The reference raises DomainError when it decodes such a byte
+      // (coding.hpp:145-148); we raise it at upload for any stored byte.
       const uint8_t* row = v->code_payload + uint64_t(src) * row_bytes;
       for (uint64_t i = 0; i < row_bytes; ++i) {
         if (invalid[row[i]]) {
@@ -247,7 +255,6 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
       }
     }
   }
-
   int prev = 0;
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
@@ -301,7 +308,7 @@ int ccq_cuda_model_info(const ccq_dev_model* m, ccq_model_info* info) {
   info->embedded_scale = m->geo.embedded_scale;
   info->payload_bytes = m->payload_bytes;
   info->device_bytes = m->device_bytes;
-  info->code_row_stride = m->code_stride;
+  info->code_row_stride = m->cgb;
   info->fast_path = m->fast ? 1 : 0;
   return CCQ_OK;
 }
