@@ -132,6 +132,24 @@ __device__ __forceinline__ float fm(uint32_t v, uint32_t one) {
   return __uint_as_float(d);
 }
 
+#ifdef CCQ_GEMV_TRACE
+}  // namespace
+__device__ unsigned long long g_trace[8192 * 8];
+namespace {
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot)                                                                    \
+  if (lane == 0) {                                                                     \
+    const int gwid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);              \
+    if (gwid < 8192) g_trace[gwid * 8 + (slot)] = gtime();                             \
+  }
+#else
+#define TRACE(slot)
+#endif
+
 struct GemvArgs {
   DevLayout L;
   const void* x;
@@ -341,6 +359,38 @@ __device__ __forceinline__ void load_x64(const void* x, int64_t base, float (&ou
   }
 }
 
+template <int XDT>
+__device__ __forceinline__ void load_x64_smem(const uint8_t* xs, int64_t base, float (&out)[64]) {
+  if constexpr (XDT == CCQ_DTYPE_F32) {
+    const uint8_t* p = xs + base * 4;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint4 v = lds128(p + 16 * i);
+      out[4 * i] = __uint_as_float(v.x);
+      out[4 * i + 1] = __uint_as_float(v.y);
+      out[4 * i + 2] = __uint_as_float(v.z);
+      out[4 * i + 3] = __uint_as_float(v.w);
+    }
+  } else {
+    const uint8_t* p = xs + base * 2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = lds128(p + 16 * i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (XDT == CCQ_DTYPE_BF16) {
+          out[8 * i + 2 * j] = __uint_as_float(w[j] << 16);
+          out[8 * i + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        } else {
+          out[8 * i + 2 * j] = __half2float(__ushort_as_half(uint16_t(w[j] & 0xFFFF)));
+          out[8 * i + 2 * j + 1] = __half2float(__ushort_as_half(uint16_t(w[j] >> 16)));
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The streaming kernel.
 // Shared memory: [partials: rows_per_cta_max][nch][MT] f32
@@ -359,62 +409,83 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   const DevLayout& L = a.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int nch = L.nch;
-  const int c = warp % nch, stream = warp / nch;
+  const int c = warp % nch;
   const int64_t rows = L.rows, gpr = L.gpr;
   const int64_t r_begin = int64_t(blockIdx.x) * rows / gridDim.x;
   const int64_t r_end = int64_t(blockIdx.x + 1) * rows / gridDim.x;
   const int nrows = int(r_end - r_begin);
-  // rows of this stream: contiguous
-  const int64_t s_begin = r_begin + int64_t(stream) * nrows / a.streams;
-  const int64_t s_end = r_begin + int64_t(stream + 1) * nrows / a.streams;
-  const int ntiles = int((s_end - s_begin + RPW - 1) / RPW);
+  const int ntiles = (nrows + RPW - 1) / RPW;  // tiles of this CTA, per chunk
 
   float* part = reinterpret_cast<float*>(smem);
   float* xs = part + ((a.rows_per_cta_max * nch * MT + 31) & ~31);
   const int64_t xstride = XREG ? 0 : gpr * T::XG;
-  uint8_t* rings = reinterpret_cast<uint8_t*>(xs + MT * xstride);
+  int* counters = reinterpret_cast<int*>(xs + MT * xstride);  // one per chunk (16 max)
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(counters + 16);
+  uint8_t* xraw = reinterpret_cast<uint8_t*>(xbar + 2);          // M = 1: x as given
+  const uint32_t xraw_bytes = XREG ? uint32_t(((L.cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2)) + 127) & ~int64_t(127)) : 0u;
+  uint8_t* rings = xraw + xraw_bytes;
   uint8_t* ring = rings + size_t(warp) * S * SB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(rings + size_t(nwarps) * S * SB) + warp * S;
 
   const int g0 = c * kChunk;
   const int ng = int(gpr - g0 < kChunk ? gpr - g0 : kChunk);
-  const uint8_t* src_codes = L.codes + (uint64_t(c) * rows) * CGB;
-  const uint8_t* src_nib = SIDE ? L.nibbles + (uint64_t(c) * rows) * 16 : nullptr;
-
-  if (lane == 0)
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-  fence_mbar_init();
-  __syncwarp();
-
-  const uint64_t pol = policy_evict_first();
-  auto issue = [&](int t) {
-    if (lane == 0) {
-      const int s = t % S;
-      const int64_t r0 = s_begin + int64_t(t) * RPW;
-      const uint32_t nr = uint32_t(s_end - r0 < RPW ? s_end - r0 : RPW);
-      uint8_t* dst = ring + s * SB;
-      mbar_arrive_expect_tx(&bars[s], nr * (CGB + (SIDE ? 32u : 0u)));
-      bulk_g2s_evict_first(dst, src_codes + r0 * CGB, nr * CGB, &bars[s], pol);
-      if constexpr (SIDE) {
-        bulk_g2s_evict_first(dst + RPW * CGB, src_nib + r0 * 16, nr * 16, &bars[s], pol);
-        bulk_g2s(dst + RPW * (CGB + 16), L.plan + r0, nr * 16, &bars[s]);
-      }
-    }
-  };
-#pragma unroll
-  for (int t = 0; t < S; ++t)
-    if (t < ntiles) issue(t);
-
-  // Activations: registers (M = 1) or shared memory (M > 1), and Q.
   const int g = g0 + lane;
   const bool active = lane < ng;
+
+  TRACE(0);
+  // 1. Activations: ONE bulk copy per CTA (not one L2 read per warp - all
+  //    SMs read the same few lines of x, which hot-spots L2 slices).
+  if (threadIdx.x < 16) counters[threadIdx.x] = 0;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+  if (threadIdx.x == 0) {
+    mbar_init(xbar, 1);
+    fence_mbar_init();
+    if constexpr (XREG) {
+      const uint32_t xb = uint32_t(L.cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2));
+      mbar_arrive_expect_tx(xbar, xb);
+      bulk_g2s(xraw, a.x, xb, xbar);
+    }
+  }
+  fence_mbar_init();
+  __syncthreads();
+
+  // 2. Tiles (RPW rows of this CTA) are handed out per chunk from a shared
+  //    counter: the chunk's warps balance dynamically.
+  const uint8_t* src_codes = L.codes + (uint64_t(c) * rows) * CGB;
+  const uint8_t* src_nib = SIDE ? L.nibbles + (uint64_t(c) * rows) * 16 : nullptr;
+  const uint64_t pol = policy_evict_first();
+  int tile_of[S];
+  auto grab_issue = [&](int s) -> int {
+    int t = 0;
+    if (lane == 0) {
+      t = atomicAdd(&counters[c], 1);
+      if (t < ntiles) {
+        const int64_t r0 = r_begin + int64_t(t) * RPW;
+        const uint32_t nr = uint32_t(r_end - r0 < RPW ? r_end - r0 : RPW);
+        uint8_t* dst = ring + s * SB;
+        mbar_arrive_expect_tx(&bars[s], nr * (CGB + (SIDE ? 32u : 0u)));
+        bulk_g2s_evict_first(dst, src_codes + r0 * CGB, nr * CGB, &bars[s], pol);
+        if constexpr (SIDE) {
+          bulk_g2s_evict_first(dst + RPW * CGB, src_nib + r0 * 16, nr * 16, &bars[s], pol);
+          bulk_g2s(dst + RPW * (CGB + 16), L.plan + r0, nr * 16, &bars[s]);
+        }
+      }
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+#pragma unroll
+  for (int s = 0; s < S; ++s) tile_of[s] = grab_issue(s);
+
+  // 3. Activations to the permuted register layout (M = 1) or shared memory.
   XGroup<FAM, XREG> xg;
   float qv[MT];
   if constexpr (XREG) {
     float xv[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) xv[i] = 0.f;
-    if (active && a.M > 0) load_x64<XDT>(a.x, int64_t(g) * 64, xv);
+    mbar_wait(xbar, 0);
+    if (active && a.M > 0) load_x64_smem<XDT>(xraw, int64_t(g) * 64, xv);
     float q = 0.f;
     float xp[T::XG];
 #pragma unroll
@@ -449,14 +520,26 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   }
   uint32_t one;
   asm volatile("mov.b32 %0, 0x3f800000;" : "=r"(one));
+  TRACE(1);
+  int ntiles_done = 0;
 
-  for (int t = 0; t < ntiles; ++t) {
-    const int s = t % S;
-    const int64_t r0 = s_begin + int64_t(t) * RPW;
+  bool more = true;
+  for (int round = 0; more; ++round) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int t = tile_of[s];
+    if (t >= ntiles) {
+      more = false;
+      break;
+    }
+    const int it = round * S + s;
+    const int64_t r0 = r_begin + int64_t(t) * RPW;
     float acc[RPW * MT];
 #pragma unroll
     for (int i = 0; i < RPW * MT; ++i) acc[i] = 0.f;
-    mbar_wait(&bars[s], uint32_t((t / S) & 1));
+    mbar_wait(&bars[s], uint32_t((it / S) & 1));
+    if (it == 0) { TRACE(2); }
+    ++ntiles_done;
     const uint8_t* st = ring + s * SB;
     if (active) {
 #pragma unroll
@@ -497,7 +580,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     }
     __syncwarp();
     fence_proxy_async_smem();
-    if (t + S < ntiles) issue(t + S);
+    tile_of[s] = grab_issue(s);
 
     // Chunk partial of each (row, token): one multi-value warp reduction.
     const float v = reduce_multi<RPW * MT>(acc, lane);
@@ -505,9 +588,17 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     if ((lane & (SPAN - 1)) == 0) {
       const int idx = lane / SPAN;
       const int r = idx / MT, m = idx % MT;
-      if (r0 + r < s_end) part[(int(r0 + r - r_begin) * nch + c) * MT + m] = v;
+      if (r0 + r < r_end) part[(int(r0 + r - r_begin) * nch + c) * MT + m] = v;
     }
   }
+  }
+  TRACE(3);
+#ifdef CCQ_GEMV_TRACE
+  if (lane == 0) {
+    const int gwid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gwid < 8192) g_trace[gwid * 8 + 5] = ntiles_done;
+  }
+#endif
   __syncthreads();
   // Sum chunk partials in a fixed order; scale by the row super scale.
   for (int e = threadIdx.x; e < nrows * MT; e += blockDim.x) {
@@ -522,6 +613,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     else
       static_cast<__nv_bfloat16*>(a.y)[int64_t(m) * a.y_stride + row] = __float2bfloat16_rn(v);
   }
+  TRACE(4);
 }
 
 // ---------------------------------------------------------------------------
@@ -627,7 +719,8 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   const int warps = m->nch * a.streams;
   const size_t xbytes = MT == 1 ? 0 : size_t(MT) * m->gpr * T::XG * 4;
   const size_t pbytes = size_t((a.rows_per_cta_max * m->nch * MT + 31) & ~31) * 4;
-  const size_t smem = pbytes + xbytes + size_t(warps) * S * SB + size_t(warps) * S * 8 + 128;
+  const size_t xraw = MT == 1 ? size_t((m->cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2) + 127) & ~int64_t(127)) : 0;
+  const size_t smem = pbytes + xbytes + 64 + 16 + xraw + size_t(warps) * S * SB + size_t(warps) * S * 8 + 128;
   if (smem > size_t(max_smem)) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");
   auto kern = gemv_stream<FAM, RPW, MT, S, XDT>;
   static size_t configured[3][5][5][3] = {};
@@ -667,7 +760,7 @@ int launch_fam(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
       st = launch_stream<FAM, 2, 2, 2>(m, x, x_dtype, m0, 2, y, y_dtype, s);
       m0 += 2;
     } else {
-      st = launch_stream<FAM, 4, 1, 4>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      st = launch_stream<FAM, 2, 1, 4>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       m0 += 1;
     }
     if (st != CCQ_OK) return st;
@@ -708,3 +801,10 @@ int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
 }
 
 }  // namespace ccqb
+
+#ifdef CCQ_GEMV_TRACE
+extern "C" int ccq_trace_dump(unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, ccqb::g_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -1,0 +1,39 @@
+"""Per-warp timeline of the streaming GEMV (debug build libccq_b200_trace.so)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2507_07145_b200 as P  # noqa: E402
+
+P.LIB_PATH = os.path.join(os.path.dirname(P.__file__), "libccq_b200_trace.so")
+import torch  # noqa: E402
+
+from paper_2507_07145_b200.synthetic import random_packed  # noqa: E402
+
+fam = P.FAMILIES[sys.argv[1] if len(sys.argv) > 1 else "2.06"]
+din, dout = int(sys.argv[2]) if len(sys.argv) > 2 else 4096, int(sys.argv[3]) if len(sys.argv) > 3 else 14336
+ms = [P.DeviceModel.upload(random_packed(dout, din, fam, 64, 3 + c)) for c in range(4)]
+x = torch.randn(1, din, device="cuda").to(torch.bfloat16)
+y = torch.empty(1, dout, device="cuda")
+for r in range(3):
+    for m in ms:
+        P.matmul(m, x, out=y)
+torch.cuda.synchronize()
+buf = np.zeros(8192 * 8, np.uint64)
+assert P.lib().ccq_trace_dump(C.c_void_p(buf.ctypes.data), buf.size) == 0
+t = buf.reshape(8192, 8).astype(np.int64)
+used = t[:, 0] > 0
+t = t[used]
+base = t[:, 0].min()
+rel = (t[:, :5] - base) / 1000.0  # us
+print("warps", used.sum())
+names = ["start", "x ready", "first data", "loop end", "exit"]
+for i, n in enumerate(names):
+    col = rel[:, i]
+    print(f"{n:10s} min {col.min():7.2f}  p50 {np.median(col):7.2f}  p90 {np.percentile(col, 90):7.2f}  max {col.max():7.2f} us")
+print("tiles per warp: min", t[:, 5].min(), "max", t[:, 5].max(), "mean", t[:, 5].mean())
+loop = rel[:, 3] - rel[:, 2]
+print(f"loop time per warp: p50 {np.median(loop):.2f} max {loop.max():.2f} us; per tile p50 {np.median(loop / np.maximum(t[:, 5], 1)):.3f} us")
