@@ -248,10 +248,11 @@ def main():
 
     # --- e2e: public API, host activations in, outputs back, every layer ----
     def e2e_step():
+        # the step's inputs in (one pinned H2D), its results out (one D2H)
+        x_dev.copy_(x_host, non_blocking=True)
         for l in range(args.layers):
-            x_dev[l].copy_(x_host[l], non_blocking=True)
             P.matmul(layers[l], x_dev[l], out=y_dev[l], stream=stream)
-            y_host[l].copy_(y_dev[l], non_blocking=True)
+        y_host.copy_(y_dev, non_blocking=True)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):

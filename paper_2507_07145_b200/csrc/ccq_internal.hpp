@@ -1,20 +1,23 @@
 // Internal definitions shared by the CCQ sm_100a kernels and the C ABI.
 //
-// Device layout of an uploaded model, "chunk-major":
-//   K is cut into nch chunks of kChunk = 32 groups.  The reference stores
-//   codes group-major per row (container.hpp:44); on the device
-//     codes    [nch][rows][cgb]   cgb = round_up(32 * payload_bytes, 16)
-//              chunk c of row r holds groups 32c .. 32c+31 of the row,
-//              byte-identical to the reference payload of those groups;
-//     nibbles  [nch][rows][16]    side-band scale nibbles of the same 32
-//              groups (group j of the chunk in the low nibble of byte j/2
-//              when j is even), side-band families only;
-//     super    f32[rows]          per-row super scale (FORMAT.md §5);
-//     plan     WidenPlan[rows]    (2.06 only) exact fixed-point restatement
-//              of clustered_code_value (coding.hpp:142-150), see below.
-//   A warp working on chunk c of consecutive rows therefore reads ONE
-//   contiguous region per tile (one bulk copy each for codes, nibbles,
-//   plans).  Every chunk row starts 16-byte aligned.
+// Device layout of an uploaded model, "chunk-major records":
+//   K is cut into nch chunks of kChunk = 32 groups; rows are padded to a
+//   multiple of 16 (rows_pad).  The reference stores codes group-major per
+//   row (container.hpp:44); on the device every (chunk c, row r) pair is one
+//   self-contained, 16-byte aligned RECORD of `rec` bytes at
+//       base + (c * rows_pad + r) * rec :
+//     [0, cgb)          codes of groups 32c .. 32c+31 of row r, byte-identical
+//                       to the reference payload (cgb = round16(32 * PB));
+//     [cgb, cgb+16)     side-band scale nibbles of those groups (group j of
+//                       the chunk in the low nibble of byte j/2 when j is
+//                       even) - side-band families only;
+//     [cgb+16, cgb+32)  the row's WidenPlan - clustered family only.
+//   A warp streaming consecutive rows of one chunk therefore fetches ONE
+//   contiguous region per tile with a single bulk copy.  Padding (rows, the
+//   tail of the last chunk) is zero: zero scale codes contribute nothing.
+//     super    f32[rows_pad]       per-row super scale (FORMAT.md §5)
+//     plan     WidenPlan[rows_pad] (2.06) - same plans, row-major, for the
+//              decode kernel; see WidenPlan below.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -82,20 +85,23 @@ constexpr int kChunk = 32;  // groups per K-chunk in the device layout
 
 // Read-only view of the device layout, passed to kernels by value.
 struct DevLayout {
-  const uint8_t* codes;
-  const uint8_t* nibbles;
+  const uint8_t* codes;  // record base
   const float* super;
   const WidenPlan* plan;
-  int64_t rows, cols, gpr;
-  uint32_t cgb;  // bytes per (chunk, row)
+  int64_t rows, cols, gpr, rows_pad;
+  uint32_t cgb;  // code bytes per record
+  uint32_t rec;  // bytes per (chunk, row) record
   int nch;
   Geometry geo;
 
+  __host__ __device__ __forceinline__ const uint8_t* record(int64_t c, int64_t r) const {
+    return codes + (uint64_t(c) * rows_pad + r) * rec;
+  }
   __host__ __device__ __forceinline__ const uint8_t* group(int64_t r, int64_t gj) const {
-    return codes + (uint64_t(gj / kChunk) * rows + r) * cgb + (gj % kChunk) * geo.payload_bytes;
+    return record(gj / kChunk, r) + (gj % kChunk) * geo.payload_bytes;
   }
   __host__ __device__ __forceinline__ uint32_t nibble(int64_t r, int64_t gj) const {
-    const uint8_t b = nibbles[(uint64_t(gj / kChunk) * rows + r) * 16 + (gj % kChunk) / 2];
+    const uint8_t b = record(gj / kChunk, r)[cgb + (gj % kChunk) / 2];
     return (b >> (4 * (gj & 1))) & 0xFu;
   }
 };
@@ -111,12 +117,13 @@ struct ccq_dev_model {
 
   void* base = nullptr;
   size_t device_bytes = 0;
-  uint8_t* codes = nullptr;
-  uint8_t* nibbles = nullptr;
+  uint8_t* codes = nullptr;  // records
   float* super = nullptr;
   ccqb::WidenPlan* plan = nullptr;
-  uint32_t cgb = 0;  // bytes per (chunk, row)
-  int nch = 0;       // K chunks
+  uint32_t cgb = 0;      // code bytes per record
+  uint32_t rec = 0;      // bytes per (chunk, row) record
+  int nch = 0;           // K chunks
+  int64_t rows_pad = 0;  // rows rounded up to 16
 
   uint64_t payload_bytes = 0;  // model_payload_bytes of the reference model
   bool fast = false;           // group-64 streaming kernels apply
@@ -125,8 +132,8 @@ struct ccq_dev_model {
 namespace ccqb {
 
 inline DevLayout layout_of(const ccq_dev_model* m) {
-  return DevLayout{m->codes, m->nibbles, m->super, m->plan, m->rows, m->cols, m->gpr,
-                   m->cgb, m->nch, m->geo};
+  return DevLayout{m->codes, m->super, m->plan, m->rows, m->cols, m->gpr, m->rows_pad,
+                   m->cgb, m->rec, m->nch, m->geo};
 }
 
 // Thread-local error message + status helpers.

@@ -134,7 +134,7 @@ __device__ __forceinline__ float fm(uint32_t v, uint32_t one) {
 
 #ifdef CCQ_GEMV_TRACE
 }  // namespace
-__device__ unsigned long long g_trace[8192 * 8];
+__device__ unsigned long long g_trace[8192 * 16];
 namespace {
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -144,7 +144,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define TRACE(slot)                                                                    \
   if (lane == 0) {                                                                     \
     const int gwid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);              \
-    if (gwid < 8192) g_trace[gwid * 8 + (slot)] = gtime();                             \
+    if (gwid < 8192) g_trace[gwid * 16 + (slot)] = gtime();                             \
   }
 #else
 #define TRACE(slot)
@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   constexpr bool XREG = MT == 1;
   constexpr bool SIDE = FAM == kF206;
   constexpr int CGB = (32 * T::PB + 15) & ~15;
-  constexpr int SB = RPW * (CGB + (SIDE ? 32 : 0));
+  constexpr int REC = CGB + (SIDE ? 32 : 0);  // one (chunk, row) record
+  constexpr int SB = RPW * REC;
   extern __shared__ __align__(128) uint8_t smem[];
   const DevLayout& L = a.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -418,8 +419,9 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
 
   float* part = reinterpret_cast<float*>(smem);
   float* xs = part + ((a.rows_per_cta_max * nch * MT + 31) & ~31);
-  const int64_t xstride = XREG ? 0 : gpr * T::XG;
-  int* counters = reinterpret_cast<int*>(xs + MT * xstride);  // one per chunk (16 max)
+  const int64_t xstride = gpr * T::XG;  // floats per token (permuted, swizzled for M = 1)
+  float* qs = xs + MT * xstride;         // M = 1: Q per group
+  int* counters = reinterpret_cast<int*>(qs + (XREG ? ((gpr + 31) & ~int64_t(31)) : 0));  // one per chunk
   uint64_t* xbar = reinterpret_cast<uint64_t*>(counters + 16);
   uint8_t* xraw = reinterpret_cast<uint8_t*>(xbar + 2);          // M = 1: x as given
   const uint32_t xraw_bytes = XREG ? uint32_t(((L.cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2)) + 127) & ~int64_t(127)) : 0u;
@@ -452,8 +454,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
 
   // 2. Tiles (RPW rows of this CTA) are handed out per chunk from a shared
   //    counter: the chunk's warps balance dynamically.
-  const uint8_t* src_codes = L.codes + (uint64_t(c) * rows) * CGB;
-  const uint8_t* src_nib = SIDE ? L.nibbles + (uint64_t(c) * rows) * 16 : nullptr;
+  const uint8_t* src = L.record(c, 0);
   const uint64_t pol = policy_evict_first();
   int tile_of[S];
   auto grab_issue = [&](int s) -> int {
@@ -463,41 +464,70 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
       if (t < ntiles) {
         const int64_t r0 = r_begin + int64_t(t) * RPW;
         const uint32_t nr = uint32_t(r_end - r0 < RPW ? r_end - r0 : RPW);
-        uint8_t* dst = ring + s * SB;
-        mbar_arrive_expect_tx(&bars[s], nr * (CGB + (SIDE ? 32u : 0u)));
-        bulk_g2s_evict_first(dst, src_codes + r0 * CGB, nr * CGB, &bars[s], pol);
-        if constexpr (SIDE) {
-          bulk_g2s_evict_first(dst + RPW * CGB, src_nib + r0 * 16, nr * 16, &bars[s], pol);
-          bulk_g2s(dst + RPW * (CGB + 16), L.plan + r0, nr * 16, &bars[s]);
-        }
+        // codes (+ nibbles + plan) of nr consecutive rows: ONE bulk copy
+        mbar_arrive_expect_tx(&bars[s], nr * REC);
+        bulk_g2s_evict_first(ring + s * SB, src + r0 * REC, nr * REC, &bars[s], pol);
       }
     }
     return __shfl_sync(0xffffffffu, t, 0);
   };
+  // The activation copy goes out alone: waiting for it here (~1 us on a
+  // quiet memory system) is far cheaper than letting it queue behind the
+  // weight prefetch of every warp on the chip.
+  TRACE(6);
+  if constexpr (XREG) mbar_wait(xbar, 0);
+  TRACE(7);
 #pragma unroll
   for (int s = 0; s < S; ++s) tile_of[s] = grab_issue(s);
+  TRACE(8);
 
   // 3. Activations to the permuted register layout (M = 1) or shared memory.
   XGroup<FAM, XREG> xg;
   float qv[MT];
   if constexpr (XREG) {
-    float xv[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) xv[i] = 0.f;
-    mbar_wait(xbar, 0);
-    if (active && a.M > 0) load_x64_smem<XDT>(xraw, int64_t(g) * 64, xv);
-    float q = 0.f;
-    float xp[T::XG];
-#pragma unroll
-    for (int i = 0; i < T::XG; ++i) xp[i] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      xp[T::perm(i)] = xv[i];
-      if (!T::exact_tail(i)) q = fmaf(T::cls(i) + float(T::ZP), xv[i], q);
+    // Cooperative pass: f32, permuted per family, 16-byte chunks XOR-swizzled
+    // by (group & 15) so the per-lane register loads below are conflict-free.
+    for (int64_t e = threadIdx.x; e < gpr * 64; e += blockDim.x) {
+      const int64_t gg = e >> 6;
+      const int p = T::perm(int(e & 63));
+      const int ch = p >> 2;
+      const int pc = ch < 16 ? (ch ^ int(gg & 15)) : ch;
+      float v;
+      if constexpr (XDT == CCQ_DTYPE_F32) v = reinterpret_cast<const float*>(xraw)[e];
+      else if constexpr (XDT == CCQ_DTYPE_BF16) v = __uint_as_float(uint32_t(reinterpret_cast<const uint16_t*>(xraw)[e]) << 16);
+      else v = __half2float(reinterpret_cast<const __half*>(xraw)[e]);
+      xs[gg * T::XG + pc * 4 + (p & 3)] = v;
     }
+    TRACE(9);
+    __syncthreads();
+    TRACE(10);
+    for (int64_t gg = threadIdx.x; gg < gpr; gg += blockDim.x) {
+      float q = 0.f;
+#pragma unroll 4
+      for (int i = 0; i < 64; ++i) {
+        if (T::exact_tail(i)) continue;
+        const int p = T::perm(i), ch = p >> 2;
+        const int pc = ch < 16 ? (ch ^ int(gg & 15)) : ch;
+        q = fmaf(T::cls(i) + float(T::ZP), xs[gg * T::XG + pc * 4 + (p & 3)], q);
+      }
+      qs[gg] = q;
+    }
+    TRACE(11);
+    __syncthreads();
+    if (active && a.M > 0) {
+      const float* xp = xs + int64_t(g) * T::XG;
 #pragma unroll
-    for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(xp[4 * k], xp[4 * k + 1], xp[4 * k + 2], xp[4 * k + 3]);
-    qv[0] = q;
+      for (int k = 0; k < T::XG / 4; ++k) {
+        const int pc = k < 16 ? (k ^ (g & 15)) : k;
+        const uint4 v = lds128(xp + pc * 4);
+        xg.v[k] = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
+      }
+      qv[0] = qs[g];
+    } else {
+#pragma unroll
+      for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      qv[0] = 0.f;
+    }
   } else {
     for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr * 64; e += blockDim.x) {
       const int m = int(e / (gpr * 64));
@@ -544,12 +574,12 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     if (active) {
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-        const uint8_t* gp = st + r * CGB + lane * T::PB;
+        const uint8_t* gp = st + r * REC + lane * T::PB;
         WidenPlan pl;
         uint32_t sel[4];
         float sc206 = 0.f;
         if constexpr (SIDE) {
-          const uint4 pv = lds128(st + RPW * (CGB + 16) + r * 16);
+          const uint4 pv = lds128(st + r * REC + CGB + 16);
           pl.C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
           pl.M = pv.z;
           pl.sel = pv.w;
@@ -558,7 +588,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
           sel[1] = base + step;
           sel[2] = base + 2 * step;
           sel[3] = base + 3 * step;
-          const uint8_t nib = st[RPW * CGB + r * 16 + (lane >> 1)];
+          const uint8_t nib = st[r * REC + CGB + (lane >> 1)];
           sc206 = float((nib >> (4 * (lane & 1))) & 0xF);
         }
 #pragma unroll
@@ -596,7 +626,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
 #ifdef CCQ_GEMV_TRACE
   if (lane == 0) {
     const int gwid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (gwid < 8192) g_trace[gwid * 8 + 5] = ntiles_done;
+    if (gwid < 8192) g_trace[gwid * 16 + 5] = ntiles_done;
   }
 #endif
   __syncthreads();
@@ -696,6 +726,7 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   using T = G64<FAM>;
   constexpr int CGB = (32 * T::PB + 15) & ~15;
   constexpr int SB = RPW * (CGB + (FAM == kF206 ? 32 : 0));
+  if (m->rec != uint32_t(CGB + (FAM == kF206 ? 32 : 0))) return fail(CCQ_ERR_CONFIG, "unexpected device record size");
   GemvArgs a{};
   a.L = layout_of(m);
   const size_t xb = x_dtype == CCQ_DTYPE_F32 ? 4 : 2;
@@ -715,13 +746,18 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int64_t grid = std::min<int64_t>(sms, m->rows);
   a.rows_per_cta_max = int((m->rows + grid - 1) / grid);
-  a.streams = std::max(1, 16 / m->nch);
-  const int warps = m->nch * a.streams;
-  const size_t xbytes = MT == 1 ? 0 : size_t(MT) * m->gpr * T::XG * 4;
+  const size_t xbytes = size_t(MT) * m->gpr * T::XG * 4 + (MT == 1 ? size_t((m->gpr + 31) & ~int64_t(31)) * 4 : 0);
   const size_t pbytes = size_t((a.rows_per_cta_max * m->nch * MT + 31) & ~31) * 4;
   const size_t xraw = MT == 1 ? size_t((m->cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2) + 127) & ~int64_t(127)) : 0;
-  const size_t smem = pbytes + xbytes + 64 + 16 + xraw + size_t(warps) * S * SB + size_t(warps) * S * 8 + 128;
-  if (smem > size_t(max_smem)) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");
+  // As many row streams as the register file (16 warps) and shared memory allow.
+  size_t smem = 0;
+  int warps = 0;
+  for (a.streams = std::max(1, 16 / m->nch); a.streams >= 1; --a.streams) {
+    warps = m->nch * a.streams;
+    smem = pbytes + xbytes + 64 + 16 + xraw + size_t(warps) * S * SB + size_t(warps) * S * 8 + 128;
+    if (smem <= size_t(max_smem)) break;
+  }
+  if (a.streams < 1) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");
   auto kern = gemv_stream<FAM, RPW, MT, S, XDT>;
   static size_t configured[3][5][5][3] = {};
   size_t& conf = configured[FAM][RPW][MT][XDT];
@@ -760,7 +796,7 @@ int launch_fam(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
       st = launch_stream<FAM, 2, 2, 2>(m, x, x_dtype, m0, 2, y, y_dtype, s);
       m0 += 2;
     } else {
-      st = launch_stream<FAM, 2, 1, 4>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      st = launch_stream<FAM, 4, 1, 3>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       m0 += 1;
     }
     if (st != CCQ_OK) return st;

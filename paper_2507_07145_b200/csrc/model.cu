@@ -198,29 +198,31 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   const int64_t rows = m->rows;
   const uint64_t row_bytes = uint64_t(gpr) * geo.payload_bytes;
   m->nch = int((gpr + kChunk - 1) / kChunk);
+  m->rows_pad = (rows + 15) / 16 * 16;
   m->cgb = uint32_t(align_up(size_t(kChunk) * geo.payload_bytes, 16));
+  m->rec = m->cgb + (geo.embedded_scale ? 0u : 16u) + (fc.cluster ? 16u : 0u);
   m->payload_bytes = uint64_t(rows) * row_bytes +
                      (geo.embedded_scale ? 0 : (uint64_t(rows) * gpr + 1) / 2) + uint64_t(rows) * 4 +
                      (fc.cluster ? uint64_t(rows) * 8 : 0);
 
-  // Host staging in the chunk-major device layout (ccq_internal.hpp).
-  const size_t n_cr = size_t(m->nch) * size_t(rows);  // (chunk, row) slots
+  // Host staging in the chunk-major record layout (ccq_internal.hpp).
+  const int64_t rp = m->rows_pad;
   const size_t off_codes = 0;
-  const size_t off_nib = align_up(off_codes + n_cr * m->cgb, 256);
-  const size_t off_super = align_up(off_nib + (geo.embedded_scale ? 0 : n_cr * 16), 256);
-  const size_t off_plan = align_up(off_super + size_t(rows) * 4, 256);
-  const size_t total = align_up(off_plan + (fc.cluster ? size_t(rows) * sizeof(WidenPlan) : 0), 256) + 256;
+  const size_t off_super = align_up(off_codes + size_t(m->nch) * size_t(rp) * m->rec, 256);
+  const size_t off_plan = align_up(off_super + size_t(rp) * 4, 256);
+  const size_t total = align_up(off_plan + (fc.cluster ? size_t(rp) * sizeof(WidenPlan) : 0), 256) + 256;
   std::vector<uint8_t> host(total, 0);
+  auto rec_at = [&](int c, int64_t r) { return &host[off_codes + (size_t(c) * rp + r) * m->rec]; };
   for (int64_t r = 0; r < rows; ++r) {
     const int64_t src = r0 + r;
     for (int c = 0; c < m->nch; ++c) {
       const int64_t g0 = int64_t(c) * kChunk;
       const int64_t ng = std::min<int64_t>(kChunk, gpr - g0);
-      std::memcpy(&host[off_codes + (size_t(c) * rows + r) * m->cgb],
-                  v->code_payload + uint64_t(src) * row_bytes + uint64_t(g0) * geo.payload_bytes,
+      uint8_t* rec = rec_at(c, r);
+      std::memcpy(rec, v->code_payload + uint64_t(src) * row_bytes + uint64_t(g0) * geo.payload_bytes,
                   size_t(ng) * geo.payload_bytes);
       if (!geo.embedded_scale) {
-        uint8_t* dst = &host[off_nib + (size_t(c) * rows + r) * 16];
+        uint8_t* dst = rec + m->cgb;
         for (int64_t j = 0; j < ng; ++j) {
           const uint64_t gi = uint64_t(src) * gpr + g0 + j;
           const uint8_t nib = (v->scale_payload[gi / 2] >> (4 * (gi % 2))) & 0xF;
@@ -232,6 +234,7 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   if (rows) std::memcpy(&host[off_super], v->super_scales + r0, size_t(rows) * 4);
   if (fc.cluster) {
     auto* plans = reinterpret_cast<WidenPlan*>(&host[off_plan]);
+    for (int64_t r = rows; r < rp; ++r) plans[r] = WidenPlan{0, 0, plan_sel(0)};
     for (int64_t r = 0; r < rows; ++r) {
       bool invalid[256];
       const int64_t src = r0 + r;
@@ -254,7 +257,11 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
         }
       }
     }
+    for (int64_t r = 0; r < rp; ++r)
+      for (int c = 0; c < m->nch; ++c)
+        std::memcpy(rec_at(c, r) + m->cgb + 16, &plans[r], sizeof(WidenPlan));
   }
+
   int prev = 0;
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
@@ -269,7 +276,6 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   auto* b = static_cast<uint8_t*>(m->base);
   m->device_bytes = total;
   m->codes = b + off_codes;
-  m->nibbles = geo.embedded_scale ? nullptr : b + off_nib;
   m->super = reinterpret_cast<float*>(b + off_super);
   m->plan = fc.cluster ? reinterpret_cast<WidenPlan*>(b + off_plan) : nullptr;
   m->fast = geo.group_size == 64;

@@ -22,18 +22,19 @@ for r in range(3):
     for m in ms:
         P.matmul(m, x, out=y)
 torch.cuda.synchronize()
-buf = np.zeros(8192 * 8, np.uint64)
+buf = np.zeros(8192 * 16, np.uint64)
 assert P.lib().ccq_trace_dump(C.c_void_p(buf.ctypes.data), buf.size) == 0
-t = buf.reshape(8192, 8).astype(np.int64)
+t = buf.reshape(8192, 16).astype(np.int64)
 used = t[:, 0] > 0
 t = t[used]
 base = t[:, 0].min()
-rel = (t[:, :5] - base) / 1000.0  # us
+cols = [0, 6, 7, 8, 9, 10, 11, 1, 2, 3, 4]
+rel = (t[:, cols] - base) / 1000.0  # us
 print("warps", used.sum())
-names = ["start", "x ready", "first data", "loop end", "exit"]
+names = ["start", "init done", "x arrived", "tiles issued", "conv done", "conv sync", "Q done", "x ready", "first data", "loop end", "exit"]
 for i, n in enumerate(names):
     col = rel[:, i]
     print(f"{n:10s} min {col.min():7.2f}  p50 {np.median(col):7.2f}  p90 {np.percentile(col, 90):7.2f}  max {col.max():7.2f} us")
 print("tiles per warp: min", t[:, 5].min(), "max", t[:, 5].max(), "mean", t[:, 5].mean())
-loop = rel[:, 3] - rel[:, 2]
+loop = rel[:, 9] - rel[:, 8]
 print(f"loop time per warp: p50 {np.median(loop):.2f} max {loop.max():.2f} us; per tile p50 {np.median(loop / np.maximum(t[:, 5], 1)):.3f} us")
