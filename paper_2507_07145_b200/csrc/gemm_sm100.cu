@@ -1,13 +1,393 @@
-// Kernel (c): tcgen05 GEMM with in-shared-memory tile decode (placeholder
-// until the tcgen05 path lands).
+// Kernel (c): prefill / batched GEMM on the 5th-generation tensor cores.
+//
+// Reference: ccq::gemv_batch (kernels.cpp:152-187), Y = X W^T, computed here
+// as a real dense contraction once the batch is large enough to need one.
+//
+//   D[128 weight rows x BN tokens] (TMEM, f32) =
+//       A[128 x K] (decoded weights, f16, shared memory, K-major, no swizzle)
+//     * B[BN x K]^T (activations, f16, TMA with 128-byte swizzle)
+//
+// Warp roles (256 threads):
+//   warp 0      TMA producer: packed-code blocks (128 rows x 8 groups, 2D tensor
+//               map, 128B swizzle) and activation tiles (BN x 64 f16)
+//   warp 1      TMEM allocation; lane 0 issues tcgen05.mma (M=128, N=BN, K=16)
+//   warps 4-7   decode producers: thread r owns weight row r of the tile and
+//               turns one 64-weight group per K-block into 64 f16 values in
+//               the canonical K-major layout, then runs the epilogue
+//               (tcgen05.ld -> super scale -> y).
+//
+// Exactness (SURVEY §7 hard part 3): each A value is the exact f16
+//     sc * (s - zero_point) * 2^p
+// (|.| <= 15*32*8 has <= 9 significant bits), built with one HFMA2 from the
+// magic-exponent value 1024 + s*2^p; the matching activation is x * 2^-p,
+// exact in f16 for bf16 inputs.  Products are exact in the f32 accumulate,
+// so only the accumulation order differs from the reference.
+//
+// Activations are first converted by a tiny pre-pass to f16 in a per-family
+// permuted K order (the order in which the decoder emits weight pairs).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <mutex>
+
 #include "ccq_internal.hpp"
+#include "ptx.cuh"
+#include "tcgen05.cuh"
 
 namespace ccqb {
 
-bool gemm_supported(const ccq_dev_model*, int64_t) { return false; }
+namespace {
 
-int launch_gemm(const ccq_dev_model*, const void*, int, int64_t, void*, int, cudaStream_t) {
-  return fail(CCQ_ERR_CONFIG, "tcgen05 GEMM not available");
+constexpr int kBM = 128;        // weight rows per tile (UMMA M)
+constexpr int kBK = 64;         // K per block = one group
+constexpr int kStagesAB = 3;    // A/B ring
+constexpr int kStagesC = 2;     // packed-code ring (8 groups per stage)
+constexpr int kCodeBox = 128;   // bytes of codes per row per code stage (8 groups x 16 B)
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Activation pre-pass: x[M][K] (f32/bf16/f16) -> x16[Mpad][K] f16, permuted.
+// 2.06: within each stored byte (4 weights, fields s0..s3 at shifts 9,6,3,0)
+// the decoder emits (s3, s2*8, s1, s0*8) as two half2 -> x16 holds
+// (x3, x2/8, x1, x0/8) for every 4 consecutive K.
+// ---------------------------------------------------------------------------
+template <int FAM, int XDT>
+__global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __half* __restrict__ out,
+                                                 int64_t M, int64_t Mpad, int64_t K) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // one quad of 4 K
+  const int64_t nq = Mpad * (K / 4);
+  if (q >= nq) return;
+  const int64_t m = q / (K / 4);
+  const int64_t k0 = (q - m * (K / 4)) * 4;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (m < M) {
+    const int64_t base = m * K + k0;
+    if constexpr (XDT == CCQ_DTYPE_F32) {
+      const float4 t = *reinterpret_cast<const float4*>(static_cast<const float*>(x) + base);
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+      const uint2 t = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(x) + base);
+      const uint16_t h[4] = {uint16_t(t.x & 0xFFFF), uint16_t(t.x >> 16), uint16_t(t.y & 0xFFFF),
+                             uint16_t(t.y >> 16)};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        v[i] = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(uint32_t(h[i]) << 16)
+                                     : __half2float(__ushort_as_half(h[i]));
+    }
+  }
+  __half2 a, b;
+  if constexpr (FAM == kF206) {
+    a = __floats2half2_rn(v[3], v[2] * 0.125f);
+    b = __floats2half2_rn(v[1], v[0] * 0.125f);
+  }
+  uint2 o;
+  o.x = *reinterpret_cast<uint32_t*>(&a);
+  o.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(out + m * K + k0) = o;
+}
+
+struct GemmArgs {
+  const float* super;
+  const WidenPlan* plan;
+  void* y;
+  int y_dtype;
+  int64_t M, rows, K, rows_pad;
+  int nkb;  // K blocks (= groups per row)
+};
+
+__device__ __forceinline__ uint32_t lop_mask_or(uint32_t v, uint32_t mask, uint32_t magic) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(v), "r"(mask), "r"(magic));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t hfma2_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int A_BYTES = kBM * kBK * 2;              // 16 KB
+  static constexpr int B_BYTES = BN * kBK * 2;               // BN x 128 B
+  static constexpr int C_BYTES = kBM * kCodeBox;             // 16 KB codes
+  static constexpr int N_BYTES = kBM * 16;                   // 2 KB nibbles
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + kStagesAB * A_BYTES;  // 1024-aligned
+  static constexpr int OFF_C = OFF_B + kStagesAB * B_BYTES;
+  static constexpr int OFF_N = OFF_C + kStagesC * C_BYTES;
+  static constexpr int OFF_BAR = OFF_N + kStagesC * N_BYTES;
+  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // + alignment slack
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_206(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
+             const __grid_constant__ CUtensorMap tm_x, GemmArgs a) {
+  using SM = GemmSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
+  uint64_t* full_a = bars;                      // [kStagesAB], count 128
+  uint64_t* full_b = bars + kStagesAB;          // [kStagesAB], tx
+  uint64_t* empty = bars + 2 * kStagesAB;       // [kStagesAB], mma commit
+  uint64_t* code_full = bars + 3 * kStagesAB;   // [kStagesC], tx
+  uint64_t* code_empty = code_full + kStagesC;  // [kStagesC], count 128
+  uint64_t* tmem_full = code_empty + kStagesC;  // 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN;
+  const int64_t r0 = int64_t(blockIdx.y) * kBM;
+  const int nkb = a.nkb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesAB; ++s) {
+      mbar_init(&full_a[s], 128);
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kStagesC; ++s) {
+      mbar_init(&code_full[s], 1);
+      mbar_init(&code_empty[s], 128);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_codes);
+    prefetch_tmap(&tm_nib);
+    prefetch_tmap(&tm_x);
+  }
+  if (warp == 1) tmem_alloc<(BN < 32 ? 32 : BN)>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_d = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      for (int kb = 0; kb < nkb; ++kb) {
+        if ((kb & 7) == 0) {
+          const int cb = kb >> 3, cs = cb % kStagesC;
+          mbar_wait(&code_empty[cs], ((cb / kStagesC) + 1) & 1);
+          mbar_arrive_expect_tx(&code_full[cs], SM::C_BYTES + SM::N_BYTES);
+          const int c = kb / kChunk, jb = (kb % kChunk) / 8;
+          const int y = int(int64_t(c) * a.rows_pad + r0);
+          tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES, &tm_codes, jb * kCodeBox, y, &code_full[cs]);
+          tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
+        }
+        const int s = kb % kStagesAB;
+        mbar_wait(&empty[s], ((kb / kStagesAB) + 1) & 1);
+        mbar_arrive_expect_tx(&full_b[s], SM::B_BYTES);
+        tma_load_2d(smem + SM::OFF_B + s * SM::B_BYTES, &tm_x, kb * kBK, n0, &full_b[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kStagesAB;
+        const uint32_t ph = (kb / kStagesAB) & 1;
+        mbar_wait(&full_a[s], ph);
+        mbar_wait(&full_b[s], ph);
+        tc_fence_after();
+        const uint32_t a_base = smem_addr(smem + SM::OFF_A + s * SM::A_BYTES);
+        const uint32_t b_base = smem_addr(smem + SM::OFF_B + s * SM::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          // A: no-swizzle K-major: core matrices 8 rows x 16 B; K step = 2 core matrices.
+          const uint64_t da = smem_desc(a_base + k * 256, 128, 1024, 0);
+          // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
+          const uint64_t db = smem_desc(b_base + k * 32, 16, 1024, 2);
+          mma_f16(tmem_d, da, db, idesc, (kb | k) != 0);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+  } else if (warp >= 4) {
+    // ---------------- decode producers (+ epilogue) ----------------
+    const int r = threadIdx.x - 128;  // tile row
+    const int64_t row = r0 + r;
+    WidenPlan pl = WidenPlan{0, 0, plan_sel(0)};
+    if (row < a.rows) pl = a.plan[row];
+    const uint32_t selb = pl.sel & 0xFFFFu, step = pl.sel >> 16;
+    const uint32_t sel[4] = {selb, selb + step, selb + 2 * step, selb + 3 * step};
+    uint32_t magic, mask, shift26;
+    asm volatile("mov.b32 %0, 0x64006400;" : "=r"(magic));
+    asm volatile("mov.b32 %0, 0x01F8003F;" : "=r"(mask));
+    asm volatile("mov.b32 %0, 0x04000000;" : "=r"(shift26));
+    uint32_t nibword = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int cb = kb >> 3, cs = cb % kStagesC, j = kb & 7;
+      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
+      if (j == 0) {
+        mbar_wait(&code_full[cs], (cb / kStagesC) & 1);
+        const int jb = (kb % kChunk) / 8;
+        nibword = *reinterpret_cast<const uint32_t*>(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4);
+      }
+      const int s = kb % kStagesAB;
+      mbar_wait(&empty[s], ((kb / kStagesAB) + 1) & 1);
+      const uint4 cw = lds128(cstage + r * kCodeBox + ((j ^ (r & 7)) << 4));
+      const uint32_t sc = (nibword >> (4 * j)) & 0xFu;
+      // half2 (sc, sc) and bias (-(1024+32) sc, -(1024+256) sc), exact in f16
+      const __half2 sc2 = __hsub2(__halves2half2(__ushort_as_half(uint16_t(0x6400u | sc)),
+                                                 __ushort_as_half(uint16_t(0x6400u | sc))),
+                                  __float2half2_rn(1024.f));
+      const __half2 bias2 = __hmul2(sc2, __floats2half2_rn(-1056.f, -1280.f));
+      const uint32_t scu = *reinterpret_cast<const uint32_t*>(&sc2);
+      const uint32_t biasu = *reinterpret_cast<const uint32_t*>(&bias2);
+      uint8_t* abase = smem + SM::OFF_A + s * SM::A_BYTES + (r >> 3) * 1024 + (r & 7) * 16;
+      const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {  // 8 K per chunk = 2 stored bytes
+        uint32_t h[4];
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) {
+          const int byte = 2 * kc + bb;
+          const uint32_t qb = prmt(words[byte >> 2], 0u, sel[byte & 3]);
+          const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);  // code at [8,23)
+          const uint32_t w2 = prmt(hi, 0u, 0x2121u);                        // code | code << 16
+          const uint32_t w3 = __umulhi(w2, shift26);                         // w2 >> 6
+          h[2 * bb] = hfma2_u32(lop_mask_or(w2, mask, magic), scu, biasu);     // (s3, 8 s2)
+          h[2 * bb + 1] = hfma2_u32(lop_mask_or(w3, mask, magic), scu, biasu); // (s1, 8 s0)
+        }
+        *reinterpret_cast<uint4*>(abase + kc * 128) = make_uint4(h[0], h[1], h[2], h[3]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&full_a[s]);
+      if (j == 7 || kb == nkb - 1) mbar_arrive(&code_empty[cs]);
+    }
+
+    // ---------------- epilogue ----------------
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const float sup = row < a.rows ? a.super[row] : 0.f;
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(tmem_d + lane_base + cc * 32, v);
+      tmem_ld_wait();
+      if (row < a.rows) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int64_t n = n0 + cc * 32 + i;
+          if (n < a.M) {
+            const float out = __uint_as_float(v[i]) * sup;
+            if (a.y_dtype == CCQ_DTYPE_F32)
+              static_cast<float*>(a.y)[n * a.rows + row] = out;
+            else
+              static_cast<__nv_bfloat16*>(a.y)[n * a.rows + row] = __float2bfloat16_rn(out);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem_d);
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps via the driver entry point (no libcuda link).
+// ---------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t dim0, uint64_t dim1,
+                uint64_t stride1_bytes, uint32_t box0, uint32_t box1, CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(CCQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = fn(map, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CCQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return CCQ_OK;
+}
+
+template <int BN>
+int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+            cudaStream_t s) {
+  using SM = GemmSmem<BN>;
+  const int64_t K = m->cols;
+  const int64_t Mpad = (M + BN - 1) / BN * BN;
+  void* x16 = nullptr;
+  CCQ_CUDA_TRY(cudaMallocAsync(&x16, size_t(Mpad * K) * 2, s));
+  {
+    const int64_t nq = Mpad * (K / 4);
+    const unsigned blocks = unsigned((nq + 255) / 256);
+    if (x_dtype == CCQ_DTYPE_F32)
+      x_prepass<kF206, CCQ_DTYPE_F32><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), M, Mpad, K);
+    else if (x_dtype == CCQ_DTYPE_BF16)
+      x_prepass<kF206, CCQ_DTYPE_BF16><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), M, Mpad, K);
+    else
+      x_prepass<kF206, CCQ_DTYPE_F16><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), M, Mpad, K);
+    count_launch();
+  }
+  CUtensorMap tm_codes, tm_nib, tm_x;
+  int st = make_map_2d(&tm_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes, m->rec,
+                       uint64_t(m->nch) * m->rows_pad, m->rec, kCodeBox, kBM,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st == CCQ_OK)
+    st = make_map_2d(&tm_nib, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes + m->cgb, 16,
+                     uint64_t(m->nch) * m->rows_pad, m->rec, 16, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st == CCQ_OK)
+    st = make_map_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x16, uint64_t(K), uint64_t(Mpad),
+                     uint64_t(K) * 2, kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != CCQ_OK) {
+    cudaFreeAsync(x16, s);
+    return st;
+  }
+  GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr)};
+  auto kern = gemm_206<BN>;
+  static bool configured[4] = {};
+  if (!configured[BN / 64]) {
+    CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL));
+    configured[BN / 64] = true;
+  }
+  const dim3 grid(unsigned(Mpad / BN), unsigned((m->rows + kBM - 1) / kBM));
+  kern<<<grid, kThreads, SM::TOTAL, s>>>(tm_codes, tm_nib, tm_x, a);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(x16, s);
+  return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemm launch");
+}
+
+}  // namespace
+
+bool gemm_supported(const ccq_dev_model* m, int64_t M) {
+  (void)M;
+  return m->family == kF206 && m->geo.group_size == 64 && m->cols % 64 == 0 && m->cols > 0;
+}
+
+int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+                cudaStream_t s) {
+  if (M <= 64) return run_206<64>(m, x, x_dtype, M, y, y_dtype, s);
+  if (M <= 128) return run_206<128>(m, x, x_dtype, M, y, y_dtype, s);
+  return run_206<256>(m, x, x_dtype, M, y, y_dtype, s);
 }
 
 }  // namespace ccqb

@@ -231,3 +231,39 @@ def test_baseline_shape_full_size(oracle, ccq, cuda, fam):
     x = oracle.random_matrix(1, 4096, "gaussian", 4096 + 1)
     y = ccq.gemv_batch(d, x)
     assert rel_err(y, oracle.gemv_batch(s, x, threads=8)) < REL_TOL
+
+
+# ------------------------------------------------------------ gemm (c) tcgen05 --
+
+@pytest.mark.parametrize("shape", [(128, 512), (200, 4096), (384, 2048 + 64), (130, 14336), (64, 192)])
+@pytest.mark.parametrize("M", [9, 32, 64, 100, 128, 256, 300])
+def test_gemm_tcgen05_206_bf16(oracle, ccq, cuda, shape, M):
+    torch = cuda
+    rows, cols = shape
+    s = oracle.random_packed(rows, cols, 2, 64, seed=rows + cols + M)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = oracle.random_matrix(M, cols, "gaussian", 17 + M)
+    xb = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+    y = ccq.matmul(d, xb, kernel="gemm")
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, bf16_round(x), threads=8)
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
+
+
+def test_gemm_tcgen05_f32_input_within_contract(oracle, ccq, cuda):
+    s = oracle.random_packed(256, 1024, 2, 64, seed=3)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = oracle.random_matrix(64, 1024, "gaussian", 5)
+    y = ccq.gemv_batch(d, x)  # M = 64 dispatches to the tcgen05 GEMM
+    assert rel_err(y, oracle.gemv_batch(s, x, threads=8)) < CONTRACT_TOL
+
+
+def test_gemm_bf16_output(oracle, ccq, cuda):
+    torch = cuda
+    s = oracle.random_packed(256, 1024, 2, 64, seed=4)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = oracle.random_matrix(48, 1024, "gaussian", 6)
+    xb = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+    y = ccq.matmul(d, xb, kernel="gemm", out_dtype=torch.bfloat16)
+    want = oracle.gemv_batch(s, bf16_round(x), threads=8)
+    assert rel_err(y.float().cpu().numpy(), want) < 4e-3  # bf16 output rounding
