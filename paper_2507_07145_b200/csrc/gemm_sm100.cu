@@ -4,17 +4,20 @@
 // as a real dense contraction once the batch is large enough to need one.
 //
 //   D[128 weight rows x BN tokens] (TMEM, f32) =
-//       A[128 x K] (decoded weights, f16, shared memory, K-major, no swizzle)
-//     * B[BN x K]^T (activations, f16, TMA with 128-byte swizzle)
+//       A[128 x K] (decoded weights, f16, TMEM: row = lane, K along columns)
+//     * B[BN x K]^T (activations, f16, shared memory, TMA 128-byte swizzle)
 //
-// Warp roles (256 threads):
-//   warp 0      TMA producer: packed-code blocks (128 rows x 8 groups, 2D tensor
-//               map, 128B swizzle) and activation tiles (BN x 64 f16)
-//   warp 1      TMEM allocation; lane 0 issues tcgen05.mma (M=128, N=BN, K=16)
-//   warps 4-7   decode producers: thread r owns weight row r of the tile and
-//               turns one 64-weight group per K-block into 64 f16 values in
-//               the canonical K-major layout, then runs the epilogue
-//               (tcgen05.ld -> super scale -> y).
+// Warp roles (512 threads):
+//   warps 0-11  decode producers, 3 groups of 4 (K blocks kb % 3): thread r
+//               of a group owns weight row r of the tile (= TMEM lane r) and
+//               turns one 64-weight group into 32 f16x2 columns of the A
+//               stage with one tcgen05.st; afterwards they run the epilogue
+//               (tcgen05.ld -> super scale -> y)
+//   warp 12     TMA producer: packed-code blocks (128 rows x 8 groups, 2D
+//               tensor map, 128B swizzle) + side-band nibbles
+//   warp 13     TMA producer: activation tiles (BN x 64 f16, 128B swizzle)
+//   warp 14     TMEM allocation; lane 0 issues tcgen05.mma (M=128, N=BN,
+//               K=16, A from TMEM) and commits stages back to the producers
 //
 // Exactness (SURVEY §7 hard part 3): each A value is the exact f16
 //     sc * (s - zero_point) * 2^p
@@ -42,10 +45,18 @@ namespace {
 
 constexpr int kBM = 128;        // weight rows per tile (UMMA M)
 constexpr int kBK = 64;         // K per block = one group
-constexpr int kStagesAB = 3;    // A/B ring
-constexpr int kStagesC = 2;     // packed-code ring (8 groups per stage)
+constexpr int kStagesC = 5;     // packed-code ring (8 groups per stage)
 constexpr int kCodeBox = 128;   // bytes of codes per row per code stage (8 groups x 16 B)
-constexpr int kThreads = 256;
+constexpr int kPar = 3;         // decode warp groups (K blocks kb % kPar)
+constexpr int kDecWarps = 4 * kPar;  // x 4 TMEM lane quadrants
+constexpr int kThreads = 32 * kDecWarps + 128;
+// Warp roles: decode warps first, control warps LAST - the SM warp scheduler
+// prefers the highest warp id among eligible warps, and the single MMA
+// issuing thread must not be starved by the decode warps on its sub-partition.
+constexpr int kWarpCodes = kDecWarps;      // TMA producer: packed codes
+constexpr int kWarpB = kDecWarps + 1;      // TMA producer: activation tiles
+constexpr int kWarpMma = kDecWarps + 2;    // TMEM alloc + MMA issue
+constexpr int kACols = kBK / 2; // TMEM columns per A stage (two f16 per column)
 
 // ---------------------------------------------------------------------------
 // Activation pre-pass: x[M][K] (f32/bf16/f16) -> x16[Mpad][K] f16, permuted.
@@ -88,6 +99,17 @@ __global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __h
   *reinterpret_cast<uint2*>(out + m * K + k0) = o;
 }
 
+#ifdef CCQ_GEMM_TRACE
+}  // namespace
+__device__ unsigned long long g_gtrace[4096 * 8];
+namespace {
+__device__ __forceinline__ unsigned long long gclk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+  return t;
+}
+#endif
+
 struct GemmArgs {
   const float* super;
   const WidenPlan* plan;
@@ -109,18 +131,43 @@ __device__ __forceinline__ uint32_t hfma2_u32(uint32_t a, uint32_t b, uint32_t c
   return d;
 }
 
+// A (TMEM) / B (smem) ring depth: deep enough to cover the L2 latency of an
+// activation tile; the B stage is BN x 128 B.
+//
+// Rings: the decoded A tile lives in TMEM (tcgen05.st by the decode warps;
+// the MMA reads A from tensor memory, "TS" form - no shared-memory writes or
+// proxy fences; measured: same MMA rate as SS at N = 64..256).  A (TMEM
+// columns) and B (shared memory) have SEPARATE rings and barriers so the
+// activation TMA can run far ahead of the decoders (L2 latency ~1 us).
+// One ring: stage s = {A: kACols TMEM columns, B: BN x 128 B of smem}; a
+// single `full` barrier per stage completes when the 128 decoders of that K
+// block have arrived AND the activation TMA bytes have landed, so the MMA
+// issuer waits once per K block (each mbarrier wait costs ~90 cycles).
+// A stage holds G groups (K = 64 G): each mbarrier wait + tcgen05 fence on
+// the MMA issuing thread costs ~200 cycles (measured, tools/micro/mma_loop.cu)
+// while 4 MMAs of N = 64 take ~180, so small-N tiles batch several groups per
+// wait; at N = 256 one group (512 MMA cycles) already hides it.
+template <int BN>
+constexpr int groups_per_stage() { return BN <= 64 ? 4 : (BN <= 128 ? 2 : 1); }
+template <int BN>
+constexpr int stages_a() { return BN <= 64 ? 3 : 4; }
+template <int BN>
+constexpr int stages_b() { return stages_a<BN>(); }
+
 template <int BN>
 struct GemmSmem {
-  static constexpr int A_BYTES = kBM * kBK * 2;              // 16 KB
-  static constexpr int B_BYTES = BN * kBK * 2;               // BN x 128 B
+  static constexpr int SA = stages_a<BN>();
+  static constexpr int SB = stages_b<BN>();
+  static constexpr int G = groups_per_stage<BN>();
+  static constexpr int B_BLOCK = BN * kBK * 2;               // BN x 128 B per group
+  static constexpr int B_BYTES = G * B_BLOCK;
   static constexpr int C_BYTES = kBM * kCodeBox;             // 16 KB codes
   static constexpr int N_BYTES = kBM * 16;                   // 2 KB nibbles
-  static constexpr int OFF_A = 0;
-  static constexpr int OFF_B = OFF_A + kStagesAB * A_BYTES;  // 1024-aligned
-  static constexpr int OFF_C = OFF_B + kStagesAB * B_BYTES;
+  static constexpr int OFF_B = 0;                            // 1024-aligned
+  static constexpr int OFF_C = OFF_B + SB * B_BYTES;
   static constexpr int OFF_N = OFF_C + kStagesC * C_BYTES;
   static constexpr int OFF_BAR = OFF_N + kStagesC * N_BYTES;
-  static constexpr int TOTAL = OFF_BAR + 256 + 1024;  // + alignment slack
+  static constexpr int TOTAL = OFF_BAR + 512 + 1024;  // + alignment slack
 };
 
 template <int BN>
@@ -128,14 +175,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_206(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
              const __grid_constant__ CUtensorMap tm_x, GemmArgs a) {
   using SM = GemmSmem<BN>;
+  constexpr int SA = SM::SA, SB = SM::SB, G = SM::G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
-  uint64_t* full_a = bars;                      // [kStagesAB], count 128
-  uint64_t* full_b = bars + kStagesAB;          // [kStagesAB], tx
-  uint64_t* empty = bars + 2 * kStagesAB;       // [kStagesAB], mma commit
-  uint64_t* code_full = bars + 3 * kStagesAB;   // [kStagesC], tx
-  uint64_t* code_empty = code_full + kStagesC;  // [kStagesC], count 128
+  static_assert(SA == SB, "single ring");
+  uint64_t* full = bars;                        // [SA], 128 decoders + 1 TMA arrival (+tx)
+  uint64_t* empty = full + SA;                  // [SA], mma commit
+  uint64_t* code_full = empty + SA;             // [kStagesC], tx
+  uint64_t* code_empty = code_full + kStagesC;  // [kStagesC], count 32 * kDecWarps
   uint64_t* tmem_full = code_empty + kStagesC;  // 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
@@ -145,14 +193,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb = a.nkb;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStagesAB; ++s) {
-      mbar_init(&full_a[s], 128);
-      mbar_init(&full_b[s], 1);
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&full[s], 129);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kStagesC; ++s) {
       mbar_init(&code_full[s], 1);
-      mbar_init(&code_empty[s], 128);
+      mbar_init(&code_empty[s], 32 * kDecWarps);
     }
     mbar_init(tmem_full, 1);
     fence_mbar_init();
@@ -160,59 +207,87 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tm_nib);
     prefetch_tmap(&tm_x);
   }
-  if (warp == 1) tmem_alloc<(BN < 32 ? 32 : BN)>(tmem_slot);
+  constexpr int kTmemNeed = BN + SA * G * kACols;
+  constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
+  if (warp == kWarpMma) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_d = *tmem_slot;
+  const uint32_t tmem_d = *tmem_slot;        // accumulator: columns [0, BN)
+  const uint32_t tmem_a = tmem_d + BN;        // A stages: SA x G x kACols columns
+  const int nst = (nkb + G - 1) / G;          // pipeline stages (G groups each)
 
-  if (warp == 0) {
+  if (warp == kWarpB) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      for (int kb = 0; kb < nkb; ++kb) {
-        if ((kb & 7) == 0) {
-          const int cb = kb >> 3, cs = cb % kStagesC;
-          mbar_wait(&code_empty[cs], ((cb / kStagesC) + 1) & 1);
-          mbar_arrive_expect_tx(&code_full[cs], SM::C_BYTES + SM::N_BYTES);
-          const int c = kb / kChunk, jb = (kb % kChunk) / 8;
-          const int y = int(int64_t(c) * a.rows_pad + r0);
-          tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES, &tm_codes, jb * kCodeBox, y, &code_full[cs]);
-          tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
-        }
-        const int s = kb % kStagesAB;
-        mbar_wait(&empty[s], ((kb / kStagesAB) + 1) & 1);
-        mbar_arrive_expect_tx(&full_b[s], SM::B_BYTES);
-        tma_load_2d(smem + SM::OFF_B + s * SM::B_BYTES, &tm_x, kb * kBK, n0, &full_b[s]);
+      // ---------------- TMA producer: activation tiles ----------------
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % SB;
+        const int ng = nkb - st * G < G ? nkb - st * G : G;
+        mbar_wait(&empty[s], ((st / SB) + 1) & 1);
+        mbar_arrive_expect_tx(&full[s], uint32_t(ng) * SM::B_BLOCK);
+        for (int gg = 0; gg < ng; ++gg)
+          tma_load_2d(smem + SM::OFF_B + s * SM::B_BYTES + gg * SM::B_BLOCK, &tm_x,
+                      (st * G + gg) * kBK, n0, &full[s]);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kWarpCodes) {
+    if (lane == 0) {
+      // ---------------- TMA producer: packed codes (runs ahead on its own ring) ----
+      for (int cb = 0; cb * 8 < nkb; ++cb) {
+        const int kb = cb * 8, cs = cb % kStagesC;
+        mbar_wait(&code_empty[cs], ((cb / kStagesC) + 1) & 1);
+        mbar_arrive_expect_tx(&code_full[cs], SM::C_BYTES + SM::N_BYTES);
+        const int c = kb / kChunk, jb = (kb % kChunk) / 8;
+        const int y = int(int64_t(c) * a.rows_pad + r0);
+        tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES, &tm_codes, jb * kCodeBox, y, &code_full[cs]);
+        tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
+      }
+    }
+  } else if (warp == kWarpMma) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStagesAB;
-        const uint32_t ph = (kb / kStagesAB) & 1;
-        mbar_wait(&full_a[s], ph);
-        mbar_wait(&full_b[s], ph);
+#ifdef CCQ_GEMM_TRACE
+      unsigned long long wa = 0, wb = 0, t0m = gclk();
+#endif
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % SA;
+        const int ng = nkb - st * G < G ? nkb - st * G : G;
+#ifdef CCQ_GEMM_TRACE
+        unsigned long long ta = gclk();
+        mbar_wait(&full[s], (st / SA) & 1);
+        wa += gclk() - ta;
+#else
+        mbar_wait(&full[s], (st / SA) & 1);
+#endif
         tc_fence_after();
-        const uint32_t a_base = smem_addr(smem + SM::OFF_A + s * SM::A_BYTES);
         const uint32_t b_base = smem_addr(smem + SM::OFF_B + s * SM::B_BYTES);
+        for (int gg = 0; gg < ng; ++gg) {
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // A: no-swizzle K-major: core matrices 8 rows x 16 B; K step = 2 core matrices.
-          const uint64_t da = smem_desc(a_base + k * 256, 128, 1024, 0);
-          // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
-          const uint64_t db = smem_desc(b_base + k * 32, 16, 1024, 2);
-          mma_f16(tmem_d, da, db, idesc, (kb | k) != 0);
+          for (int k = 0; k < kBK / 16; ++k) {
+            // A from TMEM (lane = weight row, 8 columns per K = 16);
+            // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
+            const uint64_t db = smem_desc(b_base + gg * SM::B_BLOCK + k * 32, 16, 1024, 2);
+            mma_f16_ts(tmem_d, tmem_a + (s * G + gg) * kACols + k * 8, db, idesc, (st | gg | k) != 0);
+          }
         }
         mma_commit(&empty[s]);
       }
       mma_commit(tmem_full);
+#ifdef CCQ_GEMM_TRACE
+      if (blockIdx.x == 0 && blockIdx.y < 320) {
+        const int slot = (blockIdx.y * kDecWarps) * 8;
+        g_gtrace[slot + 5] = wa; g_gtrace[slot + 6] = wb; g_gtrace[slot + 7] = gclk() - t0m;
+      }
+#endif
     }
-  } else if (warp >= 4) {
+  } else if (warp < kDecWarps) {
     // ---------------- decode producers (+ epilogue) ----------------
-    const int r = threadIdx.x - 128;  // tile row
+    const int quad = warp & 3;              // TMEM lane quadrant this warp may access
+    const int parity = warp >> 2;           // K blocks kb % kPar == parity
+    const int r = quad * 32 + lane;         // tile row == TMEM lane
     const int64_t row = r0 + r;
+    const uint32_t lane_base = uint32_t(quad * 32) << 16;
     WidenPlan pl = WidenPlan{0, 0, plan_sel(0)};
     if (row < a.rows) pl = a.plan[row];
     const uint32_t selb = pl.sel & 0xFFFFu, step = pl.sel >> 16;
@@ -221,17 +296,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("mov.b32 %0, 0x64006400;" : "=r"(magic));
     asm volatile("mov.b32 %0, 0x01F8003F;" : "=r"(mask));
     asm volatile("mov.b32 %0, 0x04000000;" : "=r"(shift26));
-    uint32_t nibword = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int cb = kb >> 3, cs = cb % kStagesC, j = kb & 7;
-      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
-      if (j == 0) {
-        mbar_wait(&code_full[cs], (cb / kStagesC) & 1);
-        const int jb = (kb % kChunk) / 8;
-        nibword = *reinterpret_cast<const uint32_t*>(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4);
+#ifdef CCQ_GEMM_TRACE
+    unsigned long long t_code = 0, t_dec = 0, t_empty = 0, t_st = 0, t_prev = gclk(), t0 = t_prev;
+#define GT(var) { const unsigned long long _t = gclk(); var += _t - t_prev; t_prev = _t; }
+#else
+#define GT(var)
+#endif
+    // Code blocks are released by EVERY decode thread, in order: blocks this
+    // group never reads are first awaited (so the arrival lands in the right
+    // phase of code_empty), then released.
+    int next_rel = 0;
+    auto release_until = [&](int cb_end) {
+      for (; next_rel < cb_end; ++next_rel) {
+        const int rs = next_rel % kStagesC;
+        mbar_wait(&code_full[rs], (next_rel / kStagesC) & 1);
+        mbar_arrive(&code_empty[rs]);
       }
-      const int s = kb % kStagesAB;
-      mbar_wait(&empty[s], ((kb / kStagesAB) + 1) & 1);
+    };
+    for (int st = parity; st < nst; st += kPar) {
+      const int s = st % SA;
+      const int ng = nkb - st * G < G ? nkb - st * G : G;
+      for (int gg = 0; gg < ng; ++gg) {
+      const int kb = st * G + gg;
+      const int cb = kb >> 3, cs = cb % kStagesC, j = kb & 7;
+      release_until(cb);
+      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
+      mbar_wait(&code_full[cs], (cb / kStagesC) & 1);
+      GT(t_code);
+      const int jb = (kb % kChunk) / 8;
+      uint32_t nibword;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
+                   : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4)));
       const uint4 cw = lds128(cstage + r * kCodeBox + ((j ^ (r & 7)) << 4));
       const uint32_t sc = (nibword >> (4 * j)) & 0xFu;
       // half2 (sc, sc) and bias (-(1024+32) sc, -(1024+256) sc), exact in f16
@@ -241,42 +336,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       const __half2 bias2 = __hmul2(sc2, __floats2half2_rn(-1056.f, -1280.f));
       const uint32_t scu = *reinterpret_cast<const uint32_t*>(&sc2);
       const uint32_t biasu = *reinterpret_cast<const uint32_t*>(&bias2);
-      uint8_t* abase = smem + SM::OFF_A + s * SM::A_BYTES + (r >> 3) * 1024 + (r & 7) * 16;
       const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+      uint32_t h[32];
 #pragma unroll
-      for (int kc = 0; kc < 8; ++kc) {  // 8 K per chunk = 2 stored bytes
-        uint32_t h[4];
-#pragma unroll
-        for (int bb = 0; bb < 2; ++bb) {
-          const int byte = 2 * kc + bb;
-          const uint32_t qb = prmt(words[byte >> 2], 0u, sel[byte & 3]);
-          const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);  // code at [8,23)
-          const uint32_t w2 = prmt(hi, 0u, 0x2121u);                        // code | code << 16
-          const uint32_t w3 = __umulhi(w2, shift26);                         // w2 >> 6
-          h[2 * bb] = hfma2_u32(lop_mask_or(w2, mask, magic), scu, biasu);     // (s3, 8 s2)
-          h[2 * bb + 1] = hfma2_u32(lop_mask_or(w3, mask, magic), scu, biasu); // (s1, 8 s0)
-        }
-        *reinterpret_cast<uint4*>(abase + kc * 128) = make_uint4(h[0], h[1], h[2], h[3]);
+      for (int byte = 0; byte < 16; ++byte) {
+        const uint32_t qb = prmt(words[byte >> 2], 0u, sel[byte & 3]);
+        const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);  // code at [8,23)
+        const uint32_t w2 = prmt(hi, 0u, 0x2121u);                        // code | code << 16
+        const uint32_t w3 = __umulhi(w2, shift26);                         // w2 >> 6
+        h[2 * byte] = hfma2_u32(lop_mask_or(w2, mask, magic), scu, biasu);     // (s3, 8 s2)
+        h[2 * byte + 1] = hfma2_u32(lop_mask_or(w3, mask, magic), scu, biasu); // (s1, 8 s0)
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&full_a[s]);
-      if (j == 7 || kb == nkb - 1) mbar_arrive(&code_empty[cs]);
+      GT(t_dec);
+      if (gg == 0) {
+        mbar_wait(&empty[s], ((st / SA) + 1) & 1);
+        GT(t_empty);
+        tc_fence_after();
+      }
+      tmem_st32(tmem_a + lane_base + (s * G + gg) * kACols, h);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&full[s]);
+      GT(t_st);
     }
+    release_until((nkb + 7) >> 3);
+#ifdef CCQ_GEMM_TRACE
+    if (lane == 0 && blockIdx.x == 0 && blockIdx.y < 320) {
+      const int slot = (blockIdx.y * kDecWarps + warp) * 8;
+      g_gtrace[slot + 0] = t_code; g_gtrace[slot + 1] = t_dec; g_gtrace[slot + 2] = t_empty;
+      g_gtrace[slot + 3] = t_st; g_gtrace[slot + 4] = gclk() - t0;
+    }
+#endif
 
-    // ---------------- epilogue ----------------
+    // ---------------- epilogue: 32-column slices round-robin over the groups ----
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const float sup = row < a.rows ? a.super[row] : 0.f;
-    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
 #pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
+    for (int cc = parity * 32; cc < BN; cc += 32 * kPar) {
       uint32_t v[32];
-      tmem_ld32(tmem_d + lane_base + cc * 32, v);
+      tmem_ld32(tmem_d + lane_base + cc, v);
       tmem_ld_wait();
       if (row < a.rows) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int64_t n = n0 + cc * 32 + i;
+          const int64_t n = n0 + cc + i;
           if (n < a.M) {
             const float out = __uint_as_float(v[i]) * sup;
             if (a.y_dtype == CCQ_DTYPE_F32)
@@ -290,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<(BN < 32 ? 32 : BN)>(tmem_d);
+  if (warp == kWarpMma) tmem_dealloc<kTmemCols>(tmem_d);
 }
 
 // ---------------------------------------------------------------------------
@@ -391,3 +496,10 @@ int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
 }
 
 }  // namespace ccqb
+
+#ifdef CCQ_GEMM_TRACE
+extern "C" int ccq_gemm_trace_dump(unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, ccqb::g_gtrace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -816,8 +816,11 @@ int launch_generic(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
 
 }  // namespace
 
+// Dispatch (measured, profiles/): the CUDA-core streaming GEMV wins at M = 1;
+// from M = 2 the tcgen05 GEMM is faster where it exists (2.06).
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
-  return m->geo.group_size == 64 && M <= 8 && m->nch <= 16;
+  if (m->geo.group_size != 64 || m->nch > 16) return false;
+  return m->family == kF206 ? M <= 1 : M <= 8;
 }
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
