@@ -4,7 +4,7 @@
  * This is the drop-in boundary for the reference's inference path
  * (/root/reference/proj/core/include/ccq/kernels.hpp:36-76 and
  * container.hpp:37-99).  The reference has no FFI of its own; its operator
- * boundary is the C++ library API, which include/ccq/*.hpp re-declares on top
+ * boundary is the C++ library API, which the headers in include/ccq/ re-declare on top
  * of these entry points.  Plain pointers and sizes only: no C++ or torch
  * types cross this boundary.
  *
@@ -153,6 +153,19 @@ int ccq_cuda_gemm(const ccq_dev_model* model, const void* x, int x_dtype, int64_
 int ccq_cuda_grouped(const ccq_dev_model* const* models, int32_t num_experts,
                      const int32_t* offsets_device, const int32_t* offsets_host,
                      const void* x, int x_dtype, void* y, int y_dtype, void* stream);
+
+/* Stacked experts (the MoE path): E experts with identical shape/family
+ * uploaded into ONE device model (rows = E x rows_per_expert) so that all of
+ * them run in a single launch. */
+int ccq_cuda_experts_upload(const ccq_packed_view* views, int32_t num_experts, int device,
+                            ccq_dev_model** out);
+/* y[T x rows_per_expert] for x[T x cols], T = offsets[E] tokens laid out
+ * expert-major.  2.06: one tcgen05 grouped-GEMM launch over (expert, row tile,
+ * token tile); experts with no tokens exit at once (their weights are never
+ * read).  offsets_device/offsets_host hold the same E+1 int32 values. */
+int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t* offsets_device,
+                            const int32_t* offsets_host, const void* x, int x_dtype, void* y,
+                            int y_dtype, void* stream);
 
 /* ---- synchronous host-buffer entry points (the reference signatures) ---- */
 

@@ -32,7 +32,7 @@ __all__ = [
     "CcqError", "ConfigError", "DomainError", "ShapeError", "EncodingError", "FormatError",
     "CudaError", "FAMILIES", "PackedModel", "DeviceModel", "load_model", "dequantize", "gemv",
     "gemv_batch", "model_payload_bytes", "group_geometry", "clustered_code_value", "decode",
-    "matmul", "grouped", "lib", "LIB_PATH", "launch_count",
+    "matmul", "grouped", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -100,7 +100,8 @@ ABI_SYMBOLS = [
     "ccq_cuda_model_free", "ccq_cuda_model_info", "ccq_cuda_decode", "ccq_cuda_matmul",
     "ccq_cuda_gemv", "ccq_cuda_gemm", "ccq_cuda_grouped", "ccq_dequantize_host",
     "ccq_gemv_host", "ccq_gemv_batch_host", "ccq_model_payload_bytes", "ccq_group_geometry",
-    "ccq_clustered_code_value", "ccq_cuda_launch_count",
+    "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
+    "ccq_cuda_experts_matmul",
 ]
 
 _lib = None
@@ -131,6 +132,8 @@ def lib():
         for fn in (L.ccq_cuda_matmul, L.ccq_cuda_gemv, L.ccq_cuda_gemm):
             fn.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int, vp]
         L.ccq_cuda_grouped.argtypes = [vp, i32, vp, vp, vp, C.c_int, vp, C.c_int, vp]
+        L.ccq_cuda_experts_upload.argtypes = [vp, i32, C.c_int, C.POINTER(vp)]
+        L.ccq_cuda_experts_matmul.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_dequantize_host.argtypes = [vp, vp]
         L.ccq_gemv_host.argtypes = [vp, vp, u64, vp, u64]
         L.ccq_gemv_batch_host.argtypes = [vp, vp, i64, i64, vp, i64, i64]
@@ -374,6 +377,43 @@ def matmul(model: DeviceModel, x, out=None, kernel: str = "auto", out_dtype=None
           "gemm": lib().ccq_cuda_gemm}[kernel]
     _check(fn(model.h, x.data_ptr(), _torch_dtype_code(x), x.shape[0], out.data_ptr(),
               _torch_dtype_code(out), _stream_ptr(stream)))
+    return out
+
+
+class Experts(DeviceModel):
+    """E experts stacked in one device model (kernel (d), one launch)."""
+
+    @staticmethod
+    def upload(models, device: int = 0) -> "Experts":
+        views = (_View * len(models))()
+        keep = []
+        for i, m in enumerate(models):
+            v = m._view()
+            keep.append(v)
+            views[i] = v
+        h = C.c_void_p()
+        _check(lib().ccq_cuda_experts_upload(views, len(models), device, C.byref(h)))
+        ex = Experts(h)
+        ex.num_experts = len(models)
+        ex.rows_per_expert = models[0].rows
+        return ex
+
+
+def experts_matmul(experts: "Experts", offsets, x, out=None, out_dtype=None, stream=None):
+    """y[T, rows_per_expert] for expert-major tokens x[T, cols]."""
+    import torch
+    offs = np.ascontiguousarray(np.asarray(offsets, np.int32))
+    if offs.size != experts.num_experts + 1:
+        raise ShapeError("offsets must have num_experts+1 entries")
+    if not x.is_contiguous() or x.dim() != 2 or x.shape[1] != experts.cols or x.shape[0] < offs[-1]:
+        raise ShapeError("activations must be contiguous [offsets[-1], cols]")
+    offs_dev = torch.from_numpy(offs).to(x.device)
+    if out is None:
+        out = torch.empty(int(offs[-1]), experts.rows_per_expert, dtype=out_dtype or torch.float32,
+                          device=x.device)
+    _check(lib().ccq_cuda_experts_matmul(experts.h, offs_dev.data_ptr(), _np_ptr(offs), x.data_ptr(),
+                                         _torch_dtype_code(x), out.data_ptr(), _torch_dtype_code(out),
+                                         _stream_ptr(stream)))
     return out
 
 

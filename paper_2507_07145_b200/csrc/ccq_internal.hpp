@@ -126,6 +126,8 @@ struct ccq_dev_model {
   int64_t rows_pad = 0;  // rows rounded up to 16
 
   uint64_t payload_bytes = 0;  // model_payload_bytes of the reference model
+  int num_experts = 0;         // > 0: rows are num_experts stacked experts
+  int64_t rows_per_expert = 0;
   bool fast = false;           // group-64 streaming kernels apply
 };
 
@@ -154,6 +156,9 @@ int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
 int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                 int y_dtype, cudaStream_t s);
 bool gemm_supported(const ccq_dev_model* m, int64_t M);
+int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
+                        int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
+                        int y_dtype, cudaStream_t s);
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M);
 
 }  // namespace ccqb

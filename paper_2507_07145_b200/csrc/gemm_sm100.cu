@@ -59,44 +59,81 @@ constexpr int kWarpMma = kDecWarps + 2;    // TMEM alloc + MMA issue
 constexpr int kACols = kBK / 2; // TMEM columns per A stage (two f16 per column)
 
 // ---------------------------------------------------------------------------
-// Activation pre-pass: x[M][K] (f32/bf16/f16) -> x16[Mpad][K] f16, permuted.
+// Activation pre-pass: x[M][K] (f32/bf16/f16) -> x16[M*XS][K] f16, permuted,
+// one CTA per token.
 // 2.06: within each stored byte (4 weights, fields s0..s3 at shifts 9,6,3,0)
 // the decoder emits (s3, s2*8, s1, s0*8) as two half2 -> x16 holds
 // (x3, x2/8, x1, x0/8) for every 4 consecutive K.
+// Each token row is first scaled by a power of two 2^s that puts max|x| in
+// [2^14, 2^15) (exact; no f16 overflow, no subnormal loss); the epilogue
+// multiplies by inv_scale[token] = 2^-s.  f32 inputs are split into XS = 2
+// f16 rows, hi = f16(x) and lo = f16(x - hi) (22+ significant bits), whose
+// partial products the epilogue adds; bf16/f16 inputs are exact with XS = 1.
 // ---------------------------------------------------------------------------
-template <int FAM, int XDT>
-__global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __half* __restrict__ out,
-                                                 int64_t M, int64_t Mpad, int64_t K) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // one quad of 4 K
-  const int64_t nq = Mpad * (K / 4);
-  if (q >= nq) return;
-  const int64_t m = q / (K / 4);
-  const int64_t k0 = (q - m * (K / 4)) * 4;
-  float v[4] = {0.f, 0.f, 0.f, 0.f};
-  if (m < M) {
-    const int64_t base = m * K + k0;
-    if constexpr (XDT == CCQ_DTYPE_F32) {
-      const float4 t = *reinterpret_cast<const float4*>(static_cast<const float*>(x) + base);
-      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    } else {
-      const uint2 t = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(x) + base);
-      const uint16_t h[4] = {uint16_t(t.x & 0xFFFF), uint16_t(t.x >> 16), uint16_t(t.y & 0xFFFF),
-                             uint16_t(t.y >> 16)};
+template <int XDT>
+__device__ __forceinline__ void load4(const void* x, int64_t base, float (&v)[4]) {
+  if constexpr (XDT == CCQ_DTYPE_F32) {
+    const float4 t = *reinterpret_cast<const float4*>(static_cast<const float*>(x) + base);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    const uint2 t = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(x) + base);
+    const uint16_t h[4] = {uint16_t(t.x & 0xFFFF), uint16_t(t.x >> 16), uint16_t(t.y & 0xFFFF),
+                           uint16_t(t.y >> 16)};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        v[i] = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(uint32_t(h[i]) << 16)
-                                     : __half2float(__ushort_as_half(h[i]));
+    for (int i = 0; i < 4; ++i)
+      v[i] = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(uint32_t(h[i]) << 16)
+                                   : __half2float(__ushort_as_half(h[i]));
+  }
+}
+
+template <int FAM, int XDT, int XS>
+__global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __half* __restrict__ out,
+                                                 float* __restrict__ inv_scale, int64_t K) {
+  const int64_t m = blockIdx.x;
+  const int64_t nq = K / 4;
+  float mx = 0.f;
+  for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+    float v[4];
+    load4<XDT>(x, m * K + q * 4, v);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))));
+  }
+  __shared__ float red[8];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+  int ex = 0;
+  if (mx > 0.f && mx <= 3.0e38f) frexpf(mx, &ex);  // mx < 2^ex
+  int sh = mx > 0.f ? 15 - ex : 0;
+  sh = sh > 126 ? 126 : (sh < -126 ? -126 : sh);
+  const float scale = __int_as_float((127 + sh) << 23);
+  if (threadIdx.x == 0) inv_scale[m] = __int_as_float((127 - sh) << 23);
+  for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int64_t k0 = q * 4;
+    float v[4];
+    load4<XDT>(x, m * K + k0, v);
+    float t[4];
+    if constexpr (FAM == kF206) {
+      t[0] = v[3] * scale; t[1] = v[2] * scale * 0.125f; t[2] = v[1] * scale; t[3] = v[0] * scale * 0.125f;
+    }
+    const __half2 a = __floats2half2_rn(t[0], t[1]);
+    const __half2 b = __floats2half2_rn(t[2], t[3]);
+    uint2 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&a);
+    o.y = *reinterpret_cast<const uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(out + (m * XS) * K + k0) = o;
+    if constexpr (XS == 2) {
+      const float2 fa = __half22float2(a), fb = __half22float2(b);
+      const __half2 la = __floats2half2_rn(t[0] - fa.x, t[1] - fa.y);
+      const __half2 lb = __floats2half2_rn(t[2] - fb.x, t[3] - fb.y);
+      o.x = *reinterpret_cast<const uint32_t*>(&la);
+      o.y = *reinterpret_cast<const uint32_t*>(&lb);
+      *reinterpret_cast<uint2*>(out + (m * XS + 1) * K + k0) = o;
     }
   }
-  __half2 a, b;
-  if constexpr (FAM == kF206) {
-    a = __floats2half2_rn(v[3], v[2] * 0.125f);
-    b = __floats2half2_rn(v[1], v[0] * 0.125f);
-  }
-  uint2 o;
-  o.x = *reinterpret_cast<uint32_t*>(&a);
-  o.y = *reinterpret_cast<uint32_t*>(&b);
-  *reinterpret_cast<uint2*>(out + m * K + k0) = o;
 }
 
 #ifdef CCQ_GEMM_TRACE
@@ -117,6 +154,13 @@ struct GemmArgs {
   int y_dtype;
   int64_t M, rows, K, rows_pad;
   int nkb;  // K blocks (= groups per row)
+  // grouped-expert mode (offsets != nullptr): rows are E stacked experts of
+  // rows_e rows; expert e owns tokens [offsets[e], offsets[e+1]).
+  const int32_t* offsets;
+  int64_t rows_e;
+  int tpe;  // row tiles per expert
+  int xs;   // activation rows per token (2 = f32 hi/lo split)
+  const float* inv_scale;  // [tokens] power-of-two activation scale
 };
 
 __device__ __forceinline__ uint32_t lop_mask_or(uint32_t v, uint32_t mask, uint32_t magic) {
@@ -170,6 +214,13 @@ struct GemmSmem {
   static constexpr int TOTAL = OFF_BAR + 512 + 1024;  // + alignment slack
 };
 
+__device__ __forceinline__ void store_y(const GemmArgs& a, int64_t idx, float out) {
+  if (a.y_dtype == CCQ_DTYPE_F32)
+    static_cast<float*>(a.y)[idx] = out;
+  else
+    static_cast<__nv_bfloat16*>(a.y)[idx] = __float2bfloat16_rn(out);
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_206(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
@@ -188,8 +239,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN;
-  const int64_t r0 = int64_t(blockIdx.y) * kBM;
+  // Tile: weight rows [r0, row_end), tokens [n0, tok_end); y row stride y_ld,
+  // y column of row r is r - y_col0.
+  // The tile covers BN activation rows = BN / xs tokens.
+  int64_t r0, row_end, tok_end, y_ld, y_col0;
+  int n0;
+  const int tb = BN / a.xs;
+  if (a.offsets) {
+    const int e = blockIdx.y / a.tpe, t = blockIdx.y % a.tpe;
+    r0 = e * a.rows_e + int64_t(t) * kBM;
+    row_end = (e + 1) * a.rows_e < r0 + kBM ? (e + 1) * a.rows_e : r0 + kBM;
+    n0 = a.offsets[e] + blockIdx.x * tb;
+    tok_end = a.offsets[e + 1];
+    if (n0 >= tok_end) return;  // expert without (more) tokens: no work, no bytes
+    y_ld = a.rows_e;
+    y_col0 = e * a.rows_e;
+  } else {
+    r0 = int64_t(blockIdx.y) * kBM;
+    row_end = a.rows < r0 + kBM ? a.rows : r0 + kBM;
+    n0 = blockIdx.x * tb;
+    tok_end = a.M;
+    y_ld = a.rows;
+    y_col0 = 0;
+  }
   const int nkb = a.nkb;
 
   if (threadIdx.x == 0) {
@@ -227,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&full[s], uint32_t(ng) * SM::B_BLOCK);
         for (int gg = 0; gg < ng; ++gg)
           tma_load_2d(smem + SM::OFF_B + s * SM::B_BYTES + gg * SM::B_BLOCK, &tm_x,
-                      (st * G + gg) * kBK, n0, &full[s]);
+                      (st * G + gg) * kBK, n0 * a.xs, &full[s]);
       }
     }
   } else if (warp == kWarpCodes) {
@@ -289,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t row = r0 + r;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
     WidenPlan pl = WidenPlan{0, 0, plan_sel(0)};
-    if (row < a.rows) pl = a.plan[row];
+    if (row < row_end) pl = a.plan[row];
     const uint32_t selb = pl.sel & 0xFFFFu, step = pl.sel >> 16;
     const uint32_t sel[4] = {selb, selb + step, selb + 2 * step, selb + 3 * step};
     uint32_t magic, mask, shift26;
@@ -372,22 +444,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue: 32-column slices round-robin over the groups ----
     mbar_wait(tmem_full, 0);
     tc_fence_after();
-    const float sup = row < a.rows ? a.super[row] : 0.f;
+    const float sup = row < row_end ? a.super[row] : 0.f;
 #pragma unroll 1
     for (int cc = parity * 32; cc < BN; cc += 32 * kPar) {
       uint32_t v[32];
       tmem_ld32(tmem_d + lane_base + cc, v);
       tmem_ld_wait();
-      if (row < a.rows) {
+      if (row < row_end) {
+        if (a.xs == 1) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int64_t n = n0 + cc + i;
-          if (n < a.M) {
-            const float out = __uint_as_float(v[i]) * sup;
-            if (a.y_dtype == CCQ_DTYPE_F32)
-              static_cast<float*>(a.y)[n * a.rows + row] = out;
-            else
-              static_cast<__nv_bfloat16*>(a.y)[n * a.rows + row] = __float2bfloat16_rn(out);
+          for (int i = 0; i < 32; ++i) {
+            const int64_t n = n0 + cc + i;
+            if (n < tok_end) store_y(a, n * y_ld + (row - y_col0), __uint_as_float(v[i]) * sup * a.inv_scale[n]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int64_t n = n0 + (cc >> 1) + i;
+            if (n < tok_end)
+              store_y(a, n * y_ld + (row - y_col0),
+                      (__uint_as_float(v[2 * i]) + __uint_as_float(v[2 * i + 1])) * sup * a.inv_scale[n]);
           }
         }
       }
@@ -435,21 +511,24 @@ int make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t d
 
 template <int BN>
 int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
-            cudaStream_t s) {
+            cudaStream_t s, const int32_t* offsets_dev = nullptr, int64_t rows_e = 0, int E = 0,
+            int64_t max_tokens = 0) {
   using SM = GemmSmem<BN>;
   const int64_t K = m->cols;
-  const int64_t Mpad = (M + BN - 1) / BN * BN;
+  const bool grouped = offsets_dev != nullptr;
+  const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
+  const int64_t xrows = M * xs;  // activation rows (TMA zero-fills past the end)
   void* x16 = nullptr;
-  CCQ_CUDA_TRY(cudaMallocAsync(&x16, size_t(Mpad * K) * 2, s));
-  {
-    const int64_t nq = Mpad * (K / 4);
-    const unsigned blocks = unsigned((nq + 255) / 256);
+  CCQ_CUDA_TRY(cudaMallocAsync(&x16, size_t(xrows * K) * 2 + size_t(M) * 4 + 16, s));
+  float* inv_scale = reinterpret_cast<float*>(static_cast<uint8_t*>(x16) + size_t(xrows * K) * 2);
+  if (M > 0) {
+    const unsigned blocks = unsigned(M);
     if (x_dtype == CCQ_DTYPE_F32)
-      x_prepass<kF206, CCQ_DTYPE_F32><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), M, Mpad, K);
+      x_prepass<kF206, CCQ_DTYPE_F32, 2><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
     else if (x_dtype == CCQ_DTYPE_BF16)
-      x_prepass<kF206, CCQ_DTYPE_BF16><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), M, Mpad, K);
+      x_prepass<kF206, CCQ_DTYPE_BF16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
     else
-      x_prepass<kF206, CCQ_DTYPE_F16><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), M, Mpad, K);
+      x_prepass<kF206, CCQ_DTYPE_F16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
     count_launch();
   }
   CUtensorMap tm_codes, tm_nib, tm_x;
@@ -460,22 +539,27 @@ int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void*
     st = make_map_2d(&tm_nib, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes + m->cgb, 16,
                      uint64_t(m->nch) * m->rows_pad, m->rec, 16, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st == CCQ_OK)
-    st = make_map_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x16, uint64_t(K), uint64_t(Mpad),
-                     uint64_t(K) * 2, kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    st = make_map_2d(&tm_x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x16, uint64_t(K),
+                     uint64_t(xrows > 0 ? xrows : 1), uint64_t(K) * 2, kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != CCQ_OK) {
     cudaFreeAsync(x16, s);
     return st;
   }
-  GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr)};
+  GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
+             offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale};
   auto kern = gemm_206<BN>;
-  static bool configured[4] = {};
+  static bool configured[5] = {};
   if (!configured[BN / 64]) {
     CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL));
     configured[BN / 64] = true;
   }
-  const dim3 grid(unsigned(Mpad / BN), unsigned((m->rows + kBM - 1) / kBM));
-  kern<<<grid, kThreads, SM::TOTAL, s>>>(tm_codes, tm_nib, tm_x, a);
-  count_launch();
+  const int tb = BN / xs;
+  const dim3 grid = grouped ? dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe))
+                            : dim3(unsigned((M + tb - 1) / tb), unsigned((m->rows + kBM - 1) / kBM));
+  if (grid.x && grid.y) {
+    kern<<<grid, kThreads, SM::TOTAL, s>>>(tm_codes, tm_nib, tm_x, a);
+    count_launch();
+  }
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(x16, s);
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemm launch");
@@ -490,9 +574,24 @@ bool gemm_supported(const ccq_dev_model* m, int64_t M) {
 
 int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
-  if (M <= 64) return run_206<64>(m, x, x_dtype, M, y, y_dtype, s);
-  if (M <= 128) return run_206<128>(m, x, x_dtype, M, y, y_dtype, s);
+  const int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * M : M;  // BN is chosen on activation rows
+  if (xr <= 64) return run_206<64>(m, x, x_dtype, M, y, y_dtype, s);
+  if (xr <= 128) return run_206<128>(m, x, x_dtype, M, y, y_dtype, s);
   return run_206<256>(m, x, x_dtype, M, y, y_dtype, s);
+}
+
+// Kernel (d): all experts of a stacked model in ONE launch.  T = total tokens
+// (expert-major), max_tokens = largest per-expert token count.
+int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
+                        int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
+                        int y_dtype, cudaStream_t s) {
+  if (max_tokens <= 0 || T <= 0) return CCQ_OK;
+  const int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * max_tokens : max_tokens;
+  if (xr <= 64)
+    return run_206<64>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens);
+  if (xr <= 128)
+    return run_206<128>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens);
+  return run_206<256>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens);
 }
 
 }  // namespace ccqb

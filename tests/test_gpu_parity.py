@@ -255,7 +255,20 @@ def test_gemm_tcgen05_f32_input_within_contract(oracle, ccq, cuda):
     d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
     x = oracle.random_matrix(64, 1024, "gaussian", 5)
     y = ccq.gemv_batch(d, x)  # M = 64 dispatches to the tcgen05 GEMM
-    assert rel_err(y, oracle.gemv_batch(s, x, threads=8)) < CONTRACT_TOL
+    # f32 activations run as hi/lo f16 pairs: full f32-level accuracy
+    assert rel_err(y, oracle.gemv_batch(s, x, threads=8)) < REL_TOL
+
+
+@pytest.mark.parametrize("M", [1, 3, 31, 33, 200])
+@pytest.mark.parametrize("scale", [1.0, 1e-6, 3e5])
+def test_gemm_f32_input_scaling(oracle, ccq, cuda, M, scale):
+    """Per-token power-of-two scaling: tiny and huge activations stay exact."""
+    torch = cuda
+    s = oracle.random_packed(160, 1024, 2, 64, seed=M)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = (oracle.random_matrix(M, 1024, "gaussian", 40 + M) * np.float32(scale)).astype(np.float32)
+    y = ccq.matmul(d, torch.from_numpy(x).cuda(), kernel="gemm")
+    assert rel_err(y.cpu().numpy(), oracle.gemv_batch(s, x, threads=8)) < REL_TOL
 
 
 def test_gemm_bf16_output(oracle, ccq, cuda):
@@ -267,3 +280,75 @@ def test_gemm_bf16_output(oracle, ccq, cuda):
     y = ccq.matmul(d, xb, kernel="gemm", out_dtype=torch.bfloat16)
     want = oracle.gemv_batch(s, bf16_round(x), threads=8)
     assert rel_err(y.float().cpu().numpy(), want) < 4e-3  # bf16 output rounding
+
+
+# ------------------------------------------------------- grouped experts (d) --
+
+def _expert_case(oracle, fam, E, rows, cols, counts, seed):
+    secs = [oracle.random_packed(rows, cols, fam, 64, seed=seed * 97 + e) for e in range(E)]
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    x = oracle.random_matrix(int(offs[-1]), cols, "gaussian", seed + 5) if offs[-1] else \
+        np.zeros((0, cols), np.float32)
+    want = np.zeros((int(offs[-1]), rows), np.float32)
+    for e in range(E):
+        if counts[e]:
+            want[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], x[offs[e]:offs[e + 1]], threads=8)
+    return secs, offs, x, want
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+@pytest.mark.parametrize("counts", [[5, 0, 70, 1], [0, 0, 0, 3], [130, 64, 0, 257], [1, 1, 1, 1]])
+def test_experts_single_launch_matches_per_expert_oracle(oracle, ccq, cuda, fam, counts):
+    torch = cuda
+    E, rows, cols = len(counts), 200, 512
+    secs, offs, x, want = _expert_case(oracle, fam, E, rows, cols, counts, seed=sum(counts) + fam)
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s) for s in secs])
+    xb = torch.from_numpy(bf16_round(x)).cuda().to(torch.bfloat16)
+    wantb = np.zeros_like(want)
+    for e in range(E):
+        if counts[e]:
+            wantb[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], bf16_round(x[offs[e]:offs[e + 1]]), threads=8)
+    y = ccq.experts_matmul(ex, offs, xb)
+    assert rel_err(y.cpu().numpy(), wantb) < REL_TOL
+    y32 = ccq.experts_matmul(ex, offs, torch.from_numpy(x).cuda())
+    assert rel_err(y32.cpu().numpy(), want) < REL_TOL
+
+
+def test_experts_one_launch_and_untouched_padding(oracle, ccq, cuda):
+    torch = cuda
+    counts = [3, 0, 40, 0, 9, 0, 0, 100]
+    secs, offs, x, want = _expert_case(oracle, 2, 8, 256, 1024, counts, seed=11)
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s) for s in secs])
+    xb = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    y = torch.full((int(offs[-1]) + 1, 256), 7.0, device="cuda")
+    torch.cuda.synchronize()
+    n0 = ccq.launch_count()
+    ccq.experts_matmul(ex, offs, xb, out=y)
+    torch.cuda.synchronize()
+    assert ccq.launch_count() - n0 == 2  # activation pre-pass + one grouped GEMM
+    assert (y[-1] == 7.0).all()
+    wantb = np.zeros_like(want)
+    for e in range(8):
+        if counts[e]:
+            wantb[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], bf16_round(x[offs[e]:offs[e + 1]]), threads=8)
+    assert rel_err(y[:-1].cpu().numpy(), wantb) < REL_TOL
+
+
+def test_experts_match_list_api(oracle, ccq, cuda):
+    torch = cuda
+    counts = [17, 2, 0, 33]
+    secs, offs, x, want = _expert_case(oracle, 2, 4, 128, 256, counts, seed=2)
+    pms = [ccq.PackedModel.from_sections(s) for s in secs]
+    ex = ccq.Experts.upload(pms)
+    ds = [ccq.DeviceModel.upload(p) for p in pms]
+    xt = torch.from_numpy(x).cuda()
+    a = ccq.experts_matmul(ex, offs, xt).cpu().numpy()
+    b = ccq.grouped(ds, offs, xt).cpu().numpy()
+    assert rel_err(a, want) < REL_TOL and rel_err(b, want) < REL_TOL
+
+
+def test_experts_shape_errors(oracle, ccq, cuda):
+    s0 = oracle.random_packed(64, 128, 2, 64, seed=1)
+    s1 = oracle.random_packed(64, 192, 2, 64, seed=2)
+    with pytest.raises(ccq.ShapeError):
+        ccq.Experts.upload([ccq.PackedModel.from_sections(s0), ccq.PackedModel.from_sections(s1)])
