@@ -204,6 +204,7 @@ __device__ __forceinline__ float dot_206(const uint8_t* gp, const X& x, float q,
     for (int b = 0; b < 4; ++b) {
       const uint32_t qb = prmt(word, 0u, sel[b]);
       const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);
+      // IMAD.SHL (FMA pipe) measured faster than SHF here (tools/micro/dot_rate.cu)
       const uint32_t h2 = hi << 6;
       const float2 f01 = make_float2(fm<0x007E0000u>(hi, one), fm<0x000FC000u>(hi, one));
       const float2 f23 = make_float2(fm<0x007E0000u>(h2, one), fm<0x000FC000u>(h2, one));
@@ -415,17 +416,13 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   const int64_t r_begin = int64_t(blockIdx.x) * rows / gridDim.x;
   const int64_t r_end = int64_t(blockIdx.x + 1) * rows / gridDim.x;
   const int nrows = int(r_end - r_begin);
-  const int ntiles = (nrows + RPW - 1) / RPW;  // tiles of this CTA, per chunk
 
   float* part = reinterpret_cast<float*>(smem);
   float* xs = part + ((a.rows_per_cta_max * nch * MT + 31) & ~31);
   const int64_t xstride = gpr * T::XG;  // floats per token (permuted, swizzled for M = 1)
   float* qs = xs + MT * xstride;         // M = 1: Q per group
-  int* counters = reinterpret_cast<int*>(qs + (XREG ? ((gpr + 31) & ~int64_t(31)) : 0));  // one per chunk
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(counters + 16);
-  uint8_t* xraw = reinterpret_cast<uint8_t*>(xbar + 2);          // M = 1: x as given
-  const uint32_t xraw_bytes = XREG ? uint32_t(((L.cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2)) + 127) & ~int64_t(127)) : 0u;
-  uint8_t* rings = xraw + xraw_bytes;
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(qs + (XREG ? ((gpr + 31) & ~int64_t(31)) : 0) + 16);
+  uint8_t* rings = reinterpret_cast<uint8_t*>(xbar + 2);
   uint8_t* ring = rings + size_t(warp) * S * SB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(rings + size_t(nwarps) * S * SB) + warp * S;
 
@@ -435,85 +432,78 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   const bool active = lane < ng;
 
   TRACE(0);
-  // 1. Activations: ONE bulk copy per CTA (not one L2 read per warp - all
-  //    SMs read the same few lines of x, which hot-spots L2 slices).
-  if (threadIdx.x < 16) counters[threadIdx.x] = 0;
+  // 1. Barriers.  Activations arrive with ONE bulk copy per CTA (not one L2
+  //    read per warp - all SMs read the same few lines of x, which hot-spots
+  //    L2 slices).
   if (lane == 0)
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-  if (threadIdx.x == 0) {
-    mbar_init(xbar, 1);
-    fence_mbar_init();
-    if constexpr (XREG) {
-      const uint32_t xb = uint32_t(L.cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2));
-      mbar_arrive_expect_tx(xbar, xb);
-      bulk_g2s(xraw, a.x, xb, xbar);
-    }
-  }
   fence_mbar_init();
   __syncthreads();
 
-  // 2. Tiles (RPW rows of this CTA) are handed out per chunk from a shared
-  //    counter: the chunk's warps balance dynamically.
+  // 2. Static, balanced split: stream j of chunk c owns the contiguous rows
+  //    [w_begin, w_end) of this CTA (balanced to one row), streamed as RPW-row
+  //    tiles through the warp's S-stage ring.  Weight copies are issued BEFORE
+  //    the grid-dependency wait (PDL): they do not depend on the previous
+  //    kernel, so they overlap its tail.
+  const int stream = warp / nch;
+  const int64_t w_begin = r_begin + int64_t(stream) * nrows / a.streams;
+  const int64_t w_end = r_begin + int64_t(stream + 1) * nrows / a.streams;
+  const int ntl = int((w_end - w_begin + RPW - 1) / RPW);
   const uint8_t* src = L.record(c, 0);
   const uint64_t pol = policy_evict_first();
-  int tile_of[S];
-  auto grab_issue = [&](int s) -> int {
-    int t = 0;
-    if (lane == 0) {
-      t = atomicAdd(&counters[c], 1);
-      if (t < ntiles) {
-        const int64_t r0 = r_begin + int64_t(t) * RPW;
-        const uint32_t nr = uint32_t(r_end - r0 < RPW ? r_end - r0 : RPW);
-        // codes (+ nibbles + plan) of nr consecutive rows: ONE bulk copy
-        mbar_arrive_expect_tx(&bars[s], nr * REC);
-        bulk_g2s_evict_first(ring + s * SB, src + r0 * REC, nr * REC, &bars[s], pol);
-      }
+  auto issue = [&](int t, int s) {
+    if (lane == 0 && t < ntl) {
+      const int64_t r0 = w_begin + int64_t(t) * RPW;
+      const uint32_t nr = uint32_t(w_end - r0 < RPW ? w_end - r0 : RPW);
+      // codes (+ nibbles + plan) of nr consecutive rows: ONE bulk copy
+      mbar_arrive_expect_tx(&bars[s], nr * REC);
+      bulk_g2s_evict_first(ring + s * SB, src + r0 * REC, nr * REC, &bars[s], pol);
     }
-    return __shfl_sync(0xffffffffu, t, 0);
   };
-  // The activation copy goes out alone: waiting for it here (~1 us on a
-  // quiet memory system) is far cheaper than letting it queue behind the
-  // weight prefetch of every warp on the chip.
-  TRACE(6);
-  if constexpr (XREG) mbar_wait(xbar, 0);
-  TRACE(7);
 #pragma unroll
-  for (int s = 0; s < S; ++s) tile_of[s] = grab_issue(s);
+  for (int s = 0; s < S; ++s) issue(s, s);
   TRACE(8);
+  griddep_launch_dependents();
+  griddep_wait();  // x (and y) belong to the previous kernel from here on
+  TRACE(6);
 
   // 3. Activations to the permuted register layout (M = 1) or shared memory.
   XGroup<FAM, XREG> xg;
   float qv[MT];
   if constexpr (XREG) {
-    // Cooperative pass: f32, permuted per family, 16-byte chunks XOR-swizzled
-    // by (group & 15) so the per-lane register loads below are conflict-free.
-    for (int64_t e = threadIdx.x; e < gpr * 64; e += blockDim.x) {
-      const int64_t gg = e >> 6;
-      const int p = T::perm(int(e & 63));
-      const int ch = p >> 2;
-      const int pc = ch < 16 ? (ch ^ int(gg & 15)) : ch;
-      float v;
-      if constexpr (XDT == CCQ_DTYPE_F32) v = reinterpret_cast<const float*>(xraw)[e];
-      else if constexpr (XDT == CCQ_DTYPE_BF16) v = __uint_as_float(uint32_t(reinterpret_cast<const uint16_t*>(xraw)[e]) << 16);
-      else v = __half2float(reinterpret_cast<const __half*>(xraw)[e]);
-      xs[gg * T::XG + pc * 4 + (p & 3)] = v;
+    // Cooperative pass straight from global memory (plain loads: they do not
+    // queue behind this SM's weight bulk copies in the TMA unit): f32,
+    // permuted per family, 16-byte chunks XOR-swizzled by (group & 15) so
+    // the per-lane register loads below are conflict-free.
+    for (int qd = threadIdx.x; qd < int(gpr) * 16; qd += blockDim.x) {
+      const int gg = qd >> 4, i0 = (qd & 15) * 4;
+      float v[4];
+      const int64_t e0 = int64_t(gg) * 64 + i0;
+      if constexpr (XDT == CCQ_DTYPE_F32) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + e0));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+      } else {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(a.x) + e0));
+        const uint32_t hw[4] = {t.x & 0xFFFFu, t.x >> 16, t.y & 0xFFFFu, t.y >> 16};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          v[i] = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(hw[i] << 16) : __half2float(__ushort_as_half(uint16_t(hw[i])));
+      }
+      if constexpr (FAM == kF206) {  // identity permutation: one 16-byte store
+        const int ch = i0 >> 2;
+        *reinterpret_cast<float4*>(xs + gg * T::XG + ((ch ^ (gg & 15)) << 2)) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int p = T::perm(i0 + i), ch = p >> 2;
+          const int pc = ch < 16 ? (ch ^ (gg & 15)) : ch;
+          xs[gg * T::XG + pc * 4 + (p & 3)] = v[i];
+        }
+      }
     }
     TRACE(9);
     __syncthreads();
     TRACE(10);
-    for (int64_t gg = threadIdx.x; gg < gpr; gg += blockDim.x) {
-      float q = 0.f;
-#pragma unroll 4
-      for (int i = 0; i < 64; ++i) {
-        if (T::exact_tail(i)) continue;
-        const int p = T::perm(i), ch = p >> 2;
-        const int pc = ch < 16 ? (ch ^ int(gg & 15)) : ch;
-        q = fmaf(T::cls(i) + float(T::ZP), xs[gg * T::XG + pc * 4 + (p & 3)], q);
-      }
-      qs[gg] = q;
-    }
-    TRACE(11);
-    __syncthreads();
     if (active && a.M > 0) {
       const float* xp = xs + int64_t(g) * T::XG;
 #pragma unroll
@@ -522,12 +512,23 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
         const uint4 v = lds128(xp + pc * 4);
         xg.v[k] = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
       }
-      qv[0] = qs[g];
+      // Q = sum_i (class_i + zero_point) * x_i, from registers (4 chains)
+      float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (T::exact_tail(i)) continue;
+        const int p = T::perm(i);
+        const float4 f = xg.v[p >> 2];
+        const float xv = (p & 3) == 0 ? f.x : (p & 3) == 1 ? f.y : (p & 3) == 2 ? f.z : f.w;
+        q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xv, q4[i & 3]);
+      }
+      qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
     } else {
 #pragma unroll
       for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       qv[0] = 0.f;
     }
+    TRACE(11);
   } else {
     for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr * 64; e += blockDim.x) {
       const int m = int(e / (gpr * 64));
@@ -553,22 +554,18 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   TRACE(1);
   int ntiles_done = 0;
 
-  bool more = true;
-  for (int round = 0; more; ++round) {
+#pragma unroll 1
+  for (int t0 = 0; t0 < ntl; t0 += S) {
 #pragma unroll
   for (int s = 0; s < S; ++s) {
-    const int t = tile_of[s];
-    if (t >= ntiles) {
-      more = false;
-      break;
-    }
-    const int it = round * S + s;
-    const int64_t r0 = r_begin + int64_t(t) * RPW;
+    const int t = t0 + s;
+    if (t >= ntl) break;
+    const int64_t r0 = w_begin + int64_t(t) * RPW;
     float acc[RPW * MT];
 #pragma unroll
     for (int i = 0; i < RPW * MT; ++i) acc[i] = 0.f;
-    mbar_wait(&bars[s], uint32_t((it / S) & 1));
-    if (it == 0) { TRACE(2); }
+    mbar_wait(&bars[s], uint32_t((t / S) & 1));
+    if (t == 0) { TRACE(2); }
     ++ntiles_done;
     const uint8_t* st = ring + s * SB;
     if (active) {
@@ -608,9 +605,11 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
         }
       }
     }
-    __syncwarp();
-    fence_proxy_async_smem();
-    tile_of[s] = grab_issue(s);
+    if (t + S < ntl) {  // refill this stage with tile t + S
+      __syncwarp();
+      fence_proxy_async_smem();
+      issue(t + S, s);
+    }
 
     // Chunk partial of each (row, token): one multi-value warp reduction.
     const float v = reduce_multi<RPW * MT>(acc, lane);
@@ -618,7 +617,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     if ((lane & (SPAN - 1)) == 0) {
       const int idx = lane / SPAN;
       const int r = idx / MT, m = idx % MT;
-      if (r0 + r < r_end) part[(int(r0 + r - r_begin) * nch + c) * MT + m] = v;
+      if (r0 + r < w_end) part[(int(r0 + r - r_begin) * nch + c) * MT + m] = v;
     }
   }
   }
@@ -748,7 +747,7 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   a.rows_per_cta_max = int((m->rows + grid - 1) / grid);
   const size_t xbytes = size_t(MT) * m->gpr * T::XG * 4 + (MT == 1 ? size_t((m->gpr + 31) & ~int64_t(31)) * 4 : 0);
   const size_t pbytes = size_t((a.rows_per_cta_max * m->nch * MT + 31) & ~31) * 4;
-  const size_t xraw = MT == 1 ? size_t((m->cols * (XDT == CCQ_DTYPE_F32 ? 4 : 2) + 127) & ~int64_t(127)) : 0;
+  const size_t xraw = 0;
   // As many row streams as the register file (16 warps) and shared memory allow.
   size_t smem = 0;
   int warps = 0;
@@ -765,9 +764,22 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
     CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     conf = smem;
   }
-  kern<<<unsigned(grid), unsigned(warps * 32), smem, s>>>(a);
+  // Programmatic stream serialization: the prologue and the weight copies of
+  // this launch overlap the tail of the previous kernel in the stream (the
+  // kernel waits on griddepcontrol before touching x or y).
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(warps * 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   count_launch();
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemv launch");
 }
 

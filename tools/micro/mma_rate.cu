@@ -6,7 +6,7 @@
 #include "../../paper_2507_07145_b200/csrc/tcgen05.cuh"
 using namespace ccqb;
 
-template <int N, bool TS>
+template <int N, bool TS, int M = 128, int ND = 1>
 __global__ void bench(unsigned long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -17,13 +17,14 @@ __global__ void bench(unsigned long long* out, int iters) {
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = idesc_f16_f32(128, N);
+    const uint32_t idesc = idesc_f16_f32(M, N);
     const uint32_t a = smem_addr(smem), b = smem_addr(smem + 16384);
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       const uint64_t db = smem_desc(b, 16, 1024, 2);
-      if (TS) mma_f16_ts(tm, tm + 256, db, idesc, i > 0);
-      else mma_f16(tm, smem_desc(a, 128, 1024, 0), db, idesc, i > 0);
+      const uint32_t d = tm + (i % ND) * N;
+      if (TS) mma_f16_ts(d, tm + 256, db, idesc, i >= ND);
+      else mma_f16(d, smem_desc(a, 128, 1024, 0), db, idesc, i > 0);
     }
     mma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -34,22 +35,25 @@ __global__ void bench(unsigned long long* out, int iters) {
   if (warp == 0) tmem_dealloc<512>(tm);
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int M = 128, int ND = 1>
 void run(unsigned long long* d) {
-  auto k = bench<N, TS>;
+  auto k = bench<N, TS, M, ND>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
   k<<<1, 128, 100000>>>(d, 4096);
   cudaDeviceSynchronize();
   unsigned long long h;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("N=%3d %s: %.1f cycles per MMA (ideal %d)  err=%s\n", N, TS ? "TS" : "SS", h / 4096.0,
-         128 * N / 256, cudaGetErrorString(cudaGetLastError()));
+  printf("ND=%d M=%3d N=%3d %s: %.1f cycles per MMA (ideal %d)  err=%s\n", ND, M, N, TS ? "TS" : "SS", h / 4096.0,
+         M * N / 256, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 64);
-  run<64, false>(d); run<128, false>(d); run<256, false>(d);
-  run<64, true>(d); run<128, true>(d); run<256, true>(d);
+  run<64, true>(d); run<64, true, 128, 2>(d); run<64, true, 128, 4>(d);
+  run<16, true>(d); run<16, true, 128, 2>(d); run<16, true, 128, 4>(d); run<16, true, 128, 8>(d);
+  run<32, true, 128, 4>(d); run<32, true, 128, 8>(d);
+  run<16, false, 128, 8>(d); run<8, false, 64, 8>(d); run<16, false, 64, 8>(d);
+  run<128, true, 128, 2>(d);
   return 0;
 }

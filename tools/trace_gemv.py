@@ -31,7 +31,7 @@ base = t[:, 0].min()
 cols = [0, 6, 7, 8, 9, 10, 11, 1, 2, 3, 4]
 rel = (t[:, cols] - base) / 1000.0  # us
 print("warps", used.sum())
-names = ["start", "init done", "x arrived", "tiles issued", "conv done", "conv sync", "Q done", "x ready", "first data", "loop end", "exit"]
+names = ["start", "griddep ok", "x arrived", "tiles issued", "conv done", "conv sync", "Q done", "x ready", "first data", "loop end", "exit"]
 for i, n in enumerate(names):
     col = rel[:, i]
     print(f"{n:10s} min {col.min():7.2f}  p50 {np.median(col):7.2f}  p90 {np.percentile(col, 90):7.2f}  max {col.max():7.2f} us")
