@@ -20,6 +20,7 @@
 //              decode kernel; see WidenPlan below.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -160,6 +161,17 @@ int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const
                         int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
                         int y_dtype, cudaStream_t s);
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M);
+// Kernel (b) on the tensor pipe (gemv_mma.cu): M <= kMmaMaxTokens per launch
+// chunk, group size 64, all three families.
+constexpr int kMmaMaxTokens = 16;
+bool gemv_mma_supported(const ccq_dev_model* m, int64_t M);
+int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
+                    int y_dtype, cudaStream_t s);
+int num_sms(int device);
+
+// 2-D tensor map over a row-major byte/half matrix (gemm_sm100.cu).
+int make_map_2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t dim0, uint64_t dim1,
+                uint64_t stride1_bytes, uint32_t box0, uint32_t box1, CUtensorMapSwizzle sw);
 
 }  // namespace ccqb
 

@@ -708,16 +708,6 @@ __global__ void __launch_bounds__(256) gemv_generic(GenericArgs a) {
 }
 
 
-int num_sms(int device) {
-  static int cached[64] = {0};
-  if (device < 0 || device >= 64) return 148;
-  if (!cached[device]) {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
-    cached[device] = v > 0 ? v : 148;
-  }
-  return cached[device];
-}
 
 template <int FAM, int RPW, int MT, int S, int XDT>
 int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
@@ -828,6 +818,17 @@ int launch_generic(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
 
 }  // namespace
 
+int num_sms(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cached[device]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cached[device] = v > 0 ? v : 148;
+  }
+  return cached[device];
+}
+
 // Dispatch (measured, profiles/): the CUDA-core streaming GEMV wins at M = 1;
 // from M = 2 the tcgen05 GEMM is faster where it exists (2.06).
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
@@ -837,6 +838,8 @@ bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
+  if (x_dtype != CCQ_DTYPE_F32 && gemv_mma_supported(m, M))
+    return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, s);
   const bool fast = m->geo.group_size == 64 && m->nch <= 16;
   switch (m->family) {
     case kF275:

@@ -364,6 +364,11 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   if (M < 0) return fail(CCQ_ERR_SHAPE, "negative batch");
   int st = check_dtypes(x_dtype, y_dtype);
   if (st != CCQ_OK || M == 0 || m->rows == 0) return st;
+  // Dispatch by batch: the tensor-pipe GEMV streams the weights once for up
+  // to kMmaMaxTokens tokens; beyond that the tcgen05 GEMM (2.06) takes over.
+  const bool mma = x_dtype != CCQ_DTYPE_F32 && gemv_mma_supported(m, M);
+  if (mma && (M <= kMmaMaxTokens || !gemm_supported(m, M)))
+    return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
   if (!gemv_fast_supported(m, M) && gemm_supported(m, M))
     return launch_gemm(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
   return launch_gemv(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));

@@ -144,6 +144,54 @@ def test_gemv_bf16_device(models, oracle, ccq, cuda, fam, M):
     assert rel_err(y.cpu().numpy(), want) < REL_TOL
 
 
+@pytest.mark.parametrize("fam", [0, 1, 2])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("M", [1, 3, 8, 9, 16, 21])
+def test_gemv_tensor_pipe_bf16_all_shapes(models, oracle, ccq, cuda, fam, shape, M):
+    """The mma.sync GEMV (bf16 activations): every family, ragged rows/cols,
+    token counts across the n8 / n16 tiles and the 16-token launch chunks."""
+    torch = cuda
+    s, d = models[(fam, *shape)]
+    x = bf16_round(oracle.random_matrix(M, shape[1], "gaussian", 31 + M))
+    xb = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+    y = ccq.matmul(d, xb, kernel="gemv")
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, x, threads=8)
+    err = rel_err(y.cpu().numpy(), want)
+    assert err < REL_TOL, err
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+@pytest.mark.parametrize("scale", [1e-30, 1e-6, 1.0, 3e4, 1e30])
+def test_gemv_tensor_pipe_activation_range(models, oracle, ccq, cuda, fam, scale):
+    """Per-token power-of-two rescaling keeps f16 operands exact across the
+    whole bf16 range; tokens of very different magnitude share one launch."""
+    torch = cuda
+    s, d = models[(fam, 257, 4096)]
+    x = oracle.random_matrix(3, 4096, "gaussian", 5)
+    x[1] *= scale
+    x[2] *= 1.0 / scale if scale != 1.0 else 7.0
+    x = bf16_round(x)
+    y = ccq.matmul(d, torch.from_numpy(x).to("cuda").to(torch.bfloat16), kernel="gemv")
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, x, threads=8)
+    got = y.cpu().numpy()
+    for n in range(3):
+        assert rel_err(got[n], want[n]) < REL_TOL, (n, rel_err(got[n], want[n]))
+
+
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_gemv_tensor_pipe_f16_in_bf16_out(models, oracle, ccq, cuda, fam):
+    torch = cuda
+    s, d = models[(fam, 130, 14336)]
+    x = oracle.random_matrix(4, 14336, "gaussian", 9)
+    xh = torch.from_numpy(x).to("cuda").to(torch.float16)
+    y = ccq.matmul(d, xh, kernel="gemv", out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, xh.float().cpu().numpy(), threads=8)
+    assert rel_err(y.float().cpu().numpy(), want) < 5e-3  # bf16 output rounding
+
+
 def test_gemv_single_vector_and_shape_errors(models, oracle, ccq):
     s, d = models[(0, 33, 192)]
     x = oracle.random_matrix(1, 192, "uniform", 99)[0]
