@@ -130,6 +130,7 @@ struct ccq_dev_model {
   int num_experts = 0;         // > 0: rows are num_experts stacked experts
   int64_t rows_per_expert = 0;
   bool fast = false;           // group-64 streaming kernels apply
+  int plan_pos_min = 0;        // 2.06: smallest byte position of any real row's widening plan
 };
 
 namespace ccqb {
@@ -164,7 +165,10 @@ bool gemv_fast_supported(const ccq_dev_model* m, int64_t M);
 // Kernel (b) on the tensor pipe (gemv_mma.cu): M <= kMmaMaxTokens per launch
 // chunk, group size 64, all three families.
 constexpr int kMmaMaxTokens = 16;
+constexpr int kMmaMinTokens = 2;  // M = 1: CUDA-core streaming GEMV (gemv.cu)
 bool gemv_mma_supported(const ccq_dev_model* m, int64_t M);
+// smallest batch routed to the tensor-pipe GEMV (env CCQ_FORCE_MMA=1 -> 1, for tests)
+int mma_min_tokens();
 int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                     int y_dtype, cudaStream_t s);
 int num_sms(int device);

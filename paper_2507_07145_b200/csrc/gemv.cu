@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ccq_internal.hpp"
 #include "ptx.cuh"
@@ -798,7 +799,10 @@ int launch_fam(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
       st = launch_stream<FAM, 2, 2, 2>(m, x, x_dtype, m0, 2, y, y_dtype, s);
       m0 += 2;
     } else {
-      st = launch_stream<FAM, 4, 1, 3>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      static const int rpw = std::getenv("CCQ_GEMV_RPW") ? std::atoi(std::getenv("CCQ_GEMV_RPW")) : 4;
+      if (rpw == 2) st = launch_stream<FAM, 2, 1, 6>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      else if (rpw == 1) st = launch_stream<FAM, 1, 1, 8>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      else st = launch_stream<FAM, 4, 1, 3>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       m0 += 1;
     }
     if (st != CCQ_OK) return st;
@@ -838,7 +842,8 @@ bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
-  if (x_dtype != CCQ_DTYPE_F32 && gemv_mma_supported(m, M))
+  if (x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && M >= mma_min_tokens() &&
+      gemv_mma_supported(m, M))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, s);
   const bool fast = m->geo.group_size == 64 && m->nch <= 16;
   switch (m->family) {

@@ -52,22 +52,22 @@ namespace ccqb {
 namespace {
 
 constexpr int kRowsT = 16;    // rows per tile (MMA M)
-constexpr int kBlkG = 8;      // groups per staged K block
 constexpr uint32_t kMagic = 0x64006400u;  // f16x2 (1024, 1024)
 
 template <int FAM>
 struct MF;
 template <>
 struct MF<kF206> {
-  static constexpr int PB = 16, ZP = 32, BOX = 128, SIDE = 32;  // + nibbles/plan box
+  // 4-group K blocks (64-B box, 64-B swizzle) + nibbles/plan box
+  static constexpr int PB = 16, ZP = 32, BLK = 4, BOX = 64, SIDE = 32;
 };
 template <>
 struct MF<kF275> {
-  static constexpr int PB = 22, ZP = 8, BOX = 176, SIDE = 0;
+  static constexpr int PB = 22, ZP = 8, BLK = 8, BOX = 176, SIDE = 0;
 };
 template <>
 struct MF<kF25> {
-  static constexpr int PB = 20, ZP = 4, BOX = 160, SIDE = 0;
+  static constexpr int PB = 20, ZP = 4, BLK = 4, BOX = 80, SIDE = 0;
 };
 
 // (weight index within the group, field power p) of element e (0 = low half,
@@ -77,10 +77,8 @@ struct WP {
 };
 __host__ __device__ constexpr WP unit_wp(int fam, int c, int u, int e) {
   if (fam == kF206) {
-    // byte b = 4c + t; units (s3, 8 s2), (s1, 8 s0); shifts [9,6,3,0] -> weights 4b..4b+3
-    const int b = 4 * c + u / 2;
-    if ((u & 1) == 0) return e == 0 ? WP{4 * b + 3, 0} : WP{4 * b + 2, 3};
-    return e == 0 ? WP{4 * b + 1, 0} : WP{4 * b, 3};
+    // natural order: unit u of lane c holds weights 16c + 2u + e (p-free magic)
+    return WP{16 * c + 2 * u + e, 0};
   }
   if (fam == kF275) {
     // bytes B = 5c..5c+4; byte B: shift 4 -> 3B, shift 2 -> 3B+1, shift 0 -> 3B+2
@@ -119,6 +117,11 @@ __device__ __forceinline__ uint32_t lop_or(uint32_t v, uint32_t mask) {
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(v), "r"(mask), "r"(kMagic));
   return d;
 }
+__device__ __forceinline__ uint32_t lop_mg(uint32_t v, uint32_t mask, uint32_t magic) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(v), "r"(mask), "r"(magic));
+  return d;
+}
 __device__ __forceinline__ uint32_t ld32(const uint8_t* p) {
   return *reinterpret_cast<const uint32_t*>(p);
 }
@@ -142,19 +145,39 @@ struct RowCtx {
 
 // Decode lane c's 16 weights of group j (0..7 within the staged block) of
 // tile row `row` into 8 f16x2 units; returns the group's scale code.
-template <int FAM>
+template <int FAM, bool P2>
 __device__ __forceinline__ uint32_t decode_units(const uint8_t* tile, int row, int j, int c,
                                                  const RowCtx& rc, uint32_t (&u)[8]) {
   if constexpr (FAM == kF206) {
-    const uint32_t w = ld32(tile + row * 128 + ((j ^ (row & 7)) << 4) + 4 * c);
+    // `tile` already points at this lane's word of group j (see group())
+    (void)row; (void)j; (void)c;
+    const uint32_t w = ld32(tile);
+#if defined(CCQ_MMA_EXP) && CCQ_MMA_EXP == 2
+    // experiment: no decode, keep the load live
+#pragma unroll
+    for (int t = 0; t < 8; ++t) u[t] = w + t;
+    return (rc.nib >> (4 * j)) & 0xFu;
+#endif
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const uint32_t qb = prmt(w, 0u, rc.sel[t]);
-      const uint32_t hi = uint32_t((uint64_t(qb) * rc.M + rc.C) >> 32);  // code at [8,23)
-      const uint32_t w2 = prmt(hi, 0u, 0x2121u);                         // code | code << 16
-      const uint32_t w3 = w2 >> 6;
-      u[2 * t] = lop_or(w2, 0x01F8003Fu);      // (s3, 8 s2)
-      u[2 * t + 1] = lop_or(w3, 0x01F8003Fu);  // (s1, 8 s0)
+      const uint32_t hi = uint32_t((uint64_t(qb) * rc.M + rc.C) >> 32);
+      uint32_t w2, w3;
+      if constexpr (P2) {
+        // plan shifted down one byte: hi == code exactly; duplicate it into
+        // both halves on the FMA pipe (IMAD) instead of the ALU (PRMT), and
+        // alternate the >> 6 between the ALU (SHF) and the FMA pipe (IMAD.HI)
+        w2 = hi * 0x00010001u;
+        w3 = (t & 1) ? __umulhi(w2, 1u << 26) : (w2 >> 6);
+      } else {
+        w2 = prmt(hi, 0u, 0x2121u);  // code at [8,23): code | code << 16
+        w3 = w2 >> 6;
+      }
+      // natural K order: unit 2t = (w 4b, 4b+1) = (s0, s1), unit 2t+1 = (s2, s3);
+      // the p3 field takes magic 128 (ulp 1/8) so every unit value is
+      // offset + s exactly, with no power of two left on the activation
+      u[2 * t] = lop_mg(w3, 0x003F01F8u, 0x64005800u);
+      u[2 * t + 1] = lop_mg(w2, 0x003F01F8u, 0x64005800u);
     }
     return (rc.nib >> (4 * j)) & 0xFu;
   } else if constexpr (FAM == kF275) {
@@ -198,6 +221,24 @@ __device__ __forceinline__ uint32_t decode_units(const uint8_t* tile, int row, i
   }
 }
 
+#ifdef CCQ_GEMV_TRACE
+}  // namespace
+__device__ unsigned long long g_mtrace[4096 * 8];
+namespace {
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MTRACE(slot, val)                                                        \
+  if (lane == 0) {                                                              \
+    const int gwid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);       \
+    if (gwid < 4096) g_mtrace[gwid * 8 + (slot)] = (val);                        \
+  }
+#else
+#define MTRACE(slot, val)
+#endif
+
 struct MmaArgs {
   const float* super;
   const WidenPlan* plan;
@@ -206,37 +247,43 @@ struct MmaArgs {
   int x_dtype, y_dtype;
   int M;            // tokens in this launch chunk (<= 8 * NT)
   int64_t rows, rows_pad, gpr;
-  int nblk;         // K blocks of 8 groups per row
+  int nblk;         // K blocks of MF::BLK groups per row
   int ntiles;       // 16-row tiles
   int slots;        // partial slots per warp
   int64_t x_ld, y_ld;  // elements between token rows of x / y
   uint32_t xs_bytes;   // staged activation bytes (gpr * M * 128)
 };
 
-template <int FAM, int NT, int S, int XDT>
-__global__ void __launch_bounds__(384, 1)
+template <int FAM, int NT, int S, int XDT, bool P2>
+__global__ void __launch_bounds__(512, 1)
     gemv_mma(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_side,
              MmaArgs a) {
+  static_assert(XDT != CCQ_DTYPE_F32, "f32 activations use the CUDA-core GEMV");
   using F = MF<FAM>;
   constexpr int MP = 8 * NT;                       // padded tokens
   constexpr int CODE_B = kRowsT * F::BOX;          // code box bytes
   constexpr int SIDE_B = kRowsT * F::SIDE;         // nibble + plan box bytes
-  constexpr int STAGE = ((CODE_B + SIDE_B) + 1023) & ~1023;
+  constexpr int STAGE = ((CODE_B + SIDE_B) + 511) & ~511;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offset (not via an integer cast) so every derived pointer keeps
+  // the shared address space and compiles to LDS, not generic LD
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, c = lane & 3;
+  const int M = a.M;
+  const int gpr = int(a.gpr);
 
-  // shared memory: rings | xs | Q | partials | scale | barriers
+  // shared memory: rings | xs | -Q | partials | token scales | warp ranges | barriers
   uint8_t* rings = smem;
-  uint8_t* xs = rings + size_t(nw) * S * STAGE;                          // [gpr][M][4][32 B]
-  float* qs = reinterpret_cast<float*>(xs + a.xs_bytes);                 // [gpr][MP]
+  uint8_t* xs = rings + size_t(nw) * S * STAGE;                          // [M][gpr][4][32 B]
+  float* qs = reinterpret_cast<float*>(xs + a.xs_bytes);                 // [gpr][MP]  (-Q)
   float* part = qs + a.gpr * MP;                                         // [nw][slots][16][MP]
   float* tokscale = part + size_t(nw) * a.slots * kRowsT * MP;           // [MP] 2^-s_n
   int* tokmax = reinterpret_cast<int*>(tokscale + MP);                   // [MP]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tokmax + MP + 2) ;        // [nw][S]
-  bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
+  int* wrange = tokmax + MP;                                             // [16][2] first/last tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wrange + 64);             // [nw][S] + 1 (x copy)
   uint64_t* mybar = bars + warp * S;
+  uint64_t* xbar = bars + nw * S;
   uint8_t* ring = rings + size_t(warp) * S * STAGE;
 
   // CTA tiles and this warp's item range (tile-major items of 8-group blocks)
@@ -246,22 +293,36 @@ __global__ void __launch_bounds__(384, 1)
   const int i0 = int(int64_t(warp) * nitems / nw), i1 = int(int64_t(warp + 1) * nitems / nw);
   const int nmine = i1 - i0;
 
-  if (lane == 0)
+#ifdef CCQ_GEMV_TRACE
+  MTRACE(0, gtime());
+#endif
+  if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&mybar[s], 1);
+    wrange[2 * warp] = nmine > 0 ? i0 / a.nblk : 1 << 30;
+    wrange[2 * warp + 1] = nmine > 0 ? (i1 - 1) / a.nblk : -1;
+  }
+  if (threadIdx.x == 0) mbar_init(xbar, 1);
   if (threadIdx.x < MP) tokmax[threadIdx.x] = 0;
+  if (threadIdx.x < 32) wrange[32 + threadIdx.x] = 0;  // zero block for dead B lanes
   fence_mbar_init();
   __syncthreads();
 
-  auto issue = [&](int k) {  // item k of this warp into stage k % S
+  // item cursor for the TMA producer (lane 0): (tile, block) of item k,
+  // advanced incrementally - no divisions in the loop
+  int iss_tile = nmine > 0 ? t_begin + i0 / a.nblk : 0, iss_blk = nmine > 0 ? i0 % a.nblk : 0;
+  auto issue = [&](int k) {  // item k (the next one in order) into stage k % S
     if (lane == 0 && k < nmine) {
-      const int it = i0 + k;
-      const int tile = t_begin + it / a.nblk, blk = it % a.nblk;
-      const int chunk = blk >> 2;
-      const int ycoord = int(int64_t(chunk) * a.rows_pad + int64_t(tile) * kRowsT);
+      constexpr int BPC = kChunk / F::BLK;  // blocks per 32-group chunk
+      const int chunk = iss_blk / BPC;
+      const int ycoord = int(int64_t(chunk) * a.rows_pad + int64_t(iss_tile) * kRowsT);
       uint8_t* st = ring + (k % S) * STAGE;
       mbar_arrive_expect_tx(&mybar[k % S], uint32_t(CODE_B + SIDE_B));
-      tma_load_2d(st, &tm_codes, (blk & 3) * F::BOX, ycoord, &mybar[k % S]);
+      tma_load_2d(st, &tm_codes, (iss_blk - chunk * BPC) * F::BOX, ycoord, &mybar[k % S]);
       if constexpr (F::SIDE > 0) tma_load_2d(st + CODE_B, &tm_side, 0, ycoord, &mybar[k % S]);
+      if (++iss_blk == a.nblk) {
+        iss_blk = 0;
+        ++iss_tile;
+      }
     }
   };
   if (lane == 0) {
@@ -272,40 +333,45 @@ __global__ void __launch_bounds__(384, 1)
   for (int k = 0; k < S; ++k) issue(k);
   griddep_launch_dependents();
   griddep_wait();  // x (and y) belong to the previous kernel until here
+#ifdef CCQ_GEMV_TRACE
+  MTRACE(1, gtime());
+#endif
 
-  // ---- activations: per-token power-of-two scale, then the unit layout ----
-  const int M = a.M;
-  const int64_t K = a.gpr * 64;
+  // ---- activations: raw rows in by bulk copy, per-token power-of-two scale,
+  //      then converted IN PLACE to f16 (same byte size) ----
+  const uint32_t row_bytes = uint32_t(gpr) * 128u;
+  const uint32_t tok_stride = row_bytes + 16u;  // +16 B: tokens land in different banks
+  auto to_f32 = [](uint32_t wv, float& lo, float& hi) {
+    if constexpr (XDT == CCQ_DTYPE_BF16) {
+      lo = __uint_as_float(wv << 16);
+      hi = __uint_as_float(wv & 0xFFFF0000u);
+    } else {
+      lo = __half2float(__ushort_as_half(uint16_t(wv & 0xFFFFu)));
+      hi = __half2float(__ushort_as_half(uint16_t(wv >> 16)));
+    }
+  };
+  const int chunks = gpr * 8;  // 16-byte chunks per token
   {
+    // every thread loads 16-byte chunks of x straight from global memory,
+    // keeps a running max per token and parks the raw bytes in xs
     float mx[MP];
 #pragma unroll
     for (int n = 0; n < MP; ++n) mx[n] = 0.f;
-    for (int64_t e = int64_t(threadIdx.x) * 8; e < K; e += int64_t(blockDim.x) * 8) {
+    for (int idx = threadIdx.x; idx < chunks * M; idx += blockDim.x) {
+      const int n = idx / chunks, i = idx - n * chunks;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + int64_t(n) * a.x_ld) + i);
+      *reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16) = v;
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      float m = 0.f;
 #pragma unroll
-      for (int n = 0; n < MP; ++n) {
-        if (n >= M) break;
-        float v[8];
-        if constexpr (XDT == CCQ_DTYPE_F32) {
-          const float4 p = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + n * a.x_ld + e));
-          const float4 q = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + n * a.x_ld + e) + 1);
-          v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w; v[4] = q.x; v[5] = q.y; v[6] = q.z; v[7] = q.w;
-        } else {
-          const uint4 p = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + n * a.x_ld + e));
-          const uint32_t wv[4] = {p.x, p.y, p.z, p.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if constexpr (XDT == CCQ_DTYPE_BF16) {
-              v[2 * i] = __uint_as_float(wv[i] << 16);
-              v[2 * i + 1] = __uint_as_float(wv[i] & 0xFFFF0000u);
-            } else {
-              v[2 * i] = __half2float(__ushort_as_half(uint16_t(wv[i] & 0xFFFFu)));
-              v[2 * i + 1] = __half2float(__ushort_as_half(uint16_t(wv[i] >> 16)));
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[n] = fmaxf(mx[n], fabsf(v[i]));
+      for (int q = 0; q < 4; ++q) {
+        float lo, hi;
+        to_f32(wv[q], lo, hi);
+        m = fmaxf(m, fmaxf(fabsf(lo), fabsf(hi)));
       }
+#pragma unroll
+      for (int nn = 0; nn < MP; ++nn)
+        if (nn == n) mx[nn] = fmaxf(mx[nn], m);
     }
 #pragma unroll
     for (int n = 0; n < MP; ++n) {
@@ -317,79 +383,95 @@ __global__ void __launch_bounds__(384, 1)
     }
   }
   __syncthreads();
-  // token scale: put max|x| (times the largest 2^-p = 1) in [2^14, 2^15)
-  const int gpr = int(a.gpr);
-  // one job per (group G, token n, lane class c), c fastest: the 4 jobs of a
-  // group/token sit in one lane quad and combine their Q partials by shuffle.
-  const int njobs = gpr * M * 4;
-  for (int job0 = threadIdx.x - lane; job0 < njobs; job0 += blockDim.x) {
-    const int job = job0 + lane;
-    const bool live = job < njobs;
-    const int cc = job & 3, G = (job >> 2) / M, n = (job >> 2) % M;
-    float qpart = 0.f;
-    if (live) {
-      const float mxv = __int_as_float(tokmax[n]);
-      int ex = 0;
-      if (mxv > 0.f) frexpf(mxv, &ex);
-      int sh = mxv > 0.f ? 15 - ex : 0;
-      sh = sh > 100 ? 100 : (sh < -100 ? -100 : sh);
-      const float scale = ldexpf(1.f, sh);
-      if (G == 0 && cc == 0) tokscale[n] = ldexpf(1.f, -sh);
-      float xv[64];
-      const int64_t base = int64_t(n) * a.x_ld + int64_t(G) * 64;
-      if constexpr (XDT == CCQ_DTYPE_F32) {
+#ifdef CCQ_GEMV_TRACE
+  MTRACE(2, gtime());
+#endif
+  auto token_scale = [&](int n) {
+    const float mxv = __int_as_float(tokmax[n]);
+    int ex = 0;
+    if (mxv > 0.f) frexpf(mxv, &ex);
+    int sh = mxv > 0.f ? 15 - ex : 0;
+    return sh > 100 ? 100 : (sh < -100 ? -100 : sh);
+  };
+  if constexpr (FAM == kF206) {
+    // natural K order: one 16-byte chunk (8 weights) per thread, in place;
+    // Q of a group = 8 consecutive chunks, combined by shuffles.
+    // Q coefficients: offset (128 for even, 1024 for odd weights) + zero point
+    for (int job0 = threadIdx.x - lane; job0 < chunks * M; job0 += blockDim.x) {
+      const int idx = job0 + lane;
+      const bool live = idx < chunks * M;
+      const int n = live ? idx / chunks : 0, i = live ? idx % chunks : 0;
+      uint4* ptr = reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16);
+      float qpart = 0.f;
+      if (live) {
+        const int sh = token_scale(n);
+        const float scale = ldexpf(1.f, sh);
+        if (i == 0) tokscale[n] = ldexpf(1.f, -sh);
+        const uint4 v = *ptr;
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        uint32_t o[4];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float4 p = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + base) + i);
-          xv[4 * i] = p.x; xv[4 * i + 1] = p.y; xv[4 * i + 2] = p.z; xv[4 * i + 3] = p.w;
+        for (int q = 0; q < 4; ++q) {
+          float lo, hi;
+          to_f32(wv[q], lo, hi);
+          const __half2 h = __floats2half2_rn(lo * scale, hi * scale);
+          const float2 hf = __half22float2(h);
+          qpart = fmaf(128.f + float(F::ZP), hf.x, qpart);
+          qpart = fmaf(1024.f + float(F::ZP), hf.y, qpart);
+          o[q] = *reinterpret_cast<const uint32_t*>(&h);
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 p = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + base) + i);
-          const uint32_t wv[4] = {p.x, p.y, p.z, p.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if constexpr (XDT == CCQ_DTYPE_BF16) {
-              xv[8 * i + 2 * q] = __uint_as_float(wv[q] << 16);
-              xv[8 * i + 2 * q + 1] = __uint_as_float(wv[q] & 0xFFFF0000u);
-            } else {
-              xv[8 * i + 2 * q] = __half2float(__ushort_as_half(uint16_t(wv[q] & 0xFFFFu)));
-              xv[8 * i + 2 * q + 1] = __half2float(__ushort_as_half(uint16_t(wv[q] >> 16)));
-            }
-          }
-        }
+        *ptr = make_uint4(o[0], o[1], o[2], o[3]);
       }
-      uint32_t out[8];
-      auto stage_units = [&](auto cconst) {
-        constexpr int C = decltype(cconst)::value;
+      qpart += __shfl_xor_sync(0xffffffffu, qpart, 1);
+      qpart += __shfl_xor_sync(0xffffffffu, qpart, 2);
+      qpart += __shfl_xor_sync(0xffffffffu, qpart, 4);
+      if (live && (i & 7) == 0) qs[(i >> 3) * MP + n] = -qpart;
+    }
+  } else {
+    // permuted unit layout: one (token, group) per thread, all four lane
+    // classes (no divergence), in place (the thread owns the group's 128 B)
+    for (int job = threadIdx.x; job < gpr * M; job += blockDim.x) {
+      const int n = job / gpr, G = job % gpr;
+      uint8_t* gx = xs + size_t(n) * tok_stride + size_t(G) * 128;
+      const int sh = token_scale(n);
+      const float scale = ldexpf(1.f, sh);
+      if (G == 0) tokscale[n] = ldexpf(1.f, -sh);
+      float xv[64];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4*>(gx + 16 * i);
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) to_f32(wv[q], xv[8 * i + 2 * q], xv[8 * i + 2 * q + 1]);
+      }
+      float qsum = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t out[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          constexpr int dummy = 0;
-          (void)dummy;
-          const WP w0 = unit_wp(FAM, C, u, 0), w1 = unit_wp(FAM, C, u, 1);
+          const WP w0 = unit_wp(FAM, cc, u, 0), w1 = unit_wp(FAM, cc, u, 1);
           const __half h0 = __float2half_rn(xv[w0.w] * scale * (1.f / float(1 << w0.p)));
           const __half h1 = __float2half_rn(xv[w1.w] * scale * (1.f / float(1 << w1.p)));
-          qpart = fmaf(1024.f + float(F::ZP * (1 << w0.p)), __half2float(h0), qpart);
-          qpart = fmaf(1024.f + float(F::ZP * (1 << w1.p)), __half2float(h1), qpart);
+          qsum = fmaf(1024.f + float(F::ZP * (1 << w0.p)), __half2float(h0), qsum);
+          qsum = fmaf(1024.f + float(F::ZP * (1 << w1.p)), __half2float(h1), qsum);
           out[u] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
         }
-      };
-      switch (cc) {
-        case 0: stage_units(std::integral_constant<int, 0>{}); break;
-        case 1: stage_units(std::integral_constant<int, 1>{}); break;
-        case 2: stage_units(std::integral_constant<int, 2>{}); break;
-        default: stage_units(std::integral_constant<int, 3>{}); break;
+        uint4* dst = reinterpret_cast<uint4*>(gx + cc * 32);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
       }
-      uint4* dst = reinterpret_cast<uint4*>(xs + ((size_t(G) * M + n) * 4 + cc) * 32);
-      dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
-      dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+      qs[G * MP + n] = -qsum;
     }
-    qpart += __shfl_xor_sync(0xffffffffu, qpart, 1);
-    qpart += __shfl_xor_sync(0xffffffffu, qpart, 2);
-    if (live && cc == 0) qs[G * MP + n] = qpart;
   }
+  // tokens n in [M, MP): -Q = 0 so padded accumulator columns stay zero
+  for (int e = threadIdx.x; e < gpr * (MP - M); e += blockDim.x)
+    qs[(e / (MP - M)) * MP + M + e % (MP - M)] = 0.f;
   __syncthreads();
+#ifdef CCQ_GEMV_TRACE
+  MTRACE(3, gtime());
+  MTRACE(7, nmine);
+#endif
 
   // ---- main loop ----
   float yacc[NT][4];
@@ -405,77 +487,122 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n0 = nt * 8 + 2 * c;
-      pp[g * MP + n0] = yacc[nt][0];
-      pp[g * MP + n0 + 1] = yacc[nt][1];
-      pp[(g + 8) * MP + n0] = yacc[nt][2];
-      pp[(g + 8) * MP + n0 + 1] = yacc[nt][3];
+      *reinterpret_cast<float2*>(pp + g * MP + n0) = make_float2(yacc[nt][0], yacc[nt][1]);
+      *reinterpret_cast<float2*>(pp + (g + 8) * MP + n0) = make_float2(yacc[nt][2], yacc[nt][3]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) yacc[nt][i] = 0.f;
     }
   };
+  // this lane's B operand rows: token nb = nt*8 + g; lanes past M read a
+  // zero block (G stride 0) instead of branching
+  const uint8_t* xb[NT];
+  uint32_t gstride[NT];
+  uint8_t* zblk = reinterpret_cast<uint8_t*>(wrange + 32);  // 128 B of zeros
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int nb = nt * 8 + g;
+    const bool live = nb < M;
+    xb[nt] = live ? xs + size_t(nb) * tok_stride + c * 32 : zblk + c * 32;
+    gstride[nt] = live ? 128u : 0u;
+  }
+  const float* qlane = qs + 2 * c;
+  const int gx7 = g & 7;
 
+  // one 64-weight group: decode both rows, 4 K slices x NT token tiles of
+  // mma, then y += sc * D
+  auto group = [&](const uint8_t* st, int j, int G) {
+    uint32_t ua[8], ub[8];
+    uint32_t sca, scb;
+    if constexpr (FAM == kF206) {
+      // 64-B swizzle: 16-B chunk j of row r sits at r*64 + ((j ^ ((r >> 1) & 3)) << 4);
+      // rows g and g+8 share the XOR term, so one per-lane offset serves both
+      const uint8_t* p = st + g * 64 + ((j ^ ((g >> 1) & 3)) << 4) + 4 * c;
+      sca = decode_units<FAM, P2>(p, g, j, c, rc[0], ua);
+      scb = decode_units<FAM, P2>(p + 8 * 64, g + 8, j, c, rc[1], ub);
+    } else {
+      sca = decode_units<FAM, P2>(st, g, j, c, rc[0], ua);
+      scb = decode_units<FAM, P2>(st, g + 8, j, c, rc[1], ub);
+    }
+    const float fa = float(sca), fb = float(scb);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const float2 q2 = *reinterpret_cast<const float2*>(qlane + G * MP + nt * 8);
+      float d[4] = {q2.x, q2.y, q2.x, q2.y};
+      const uint4* src = reinterpret_cast<const uint4*>(xb[nt] + uint32_t(G) * gstride[nt]);
+      const uint4 b01 = src[0], b23 = src[1];
+      const uint32_t bb[8] = {b01.x, b01.y, b01.z, b01.w, b23.x, b23.y, b23.z, b23.w};
+      // two independent accumulator chains (slices 0,2 and 1,3): halves the
+      // dependent-mma latency per group
+      float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t af[4] = {ua[2 * t], ub[2 * t], ua[2 * t + 1], ub[2 * t + 1]};
+#if defined(CCQ_MMA_EXP) && CCQ_MMA_EXP == 1
+        // experiment: no tensor op, keep the decode live
+        d[0] += __uint_as_float(af[0] ^ bb[2 * t]); d[1] += __uint_as_float(af[1]);
+        e[2] += __uint_as_float(af[2] ^ bb[2 * t + 1]); e[3] += __uint_as_float(af[3]);
+#else
+        if (t & 1) mma16816(e, af, bb[2 * t], bb[2 * t + 1]);
+        else mma16816(d, af, bb[2 * t], bb[2 * t + 1]);
+#endif
+      }
+      yacc[nt][0] = fmaf(fa, d[0] + e[0], yacc[nt][0]);
+      yacc[nt][1] = fmaf(fa, d[1] + e[1], yacc[nt][1]);
+      yacc[nt][2] = fmaf(fb, d[2] + e[2], yacc[nt][2]);
+      yacc[nt][3] = fmaf(fb, d[3] + e[3], yacc[nt][3]);
+    }
+  };
+  (void)gx7;
+
+  int tile = cur_tile, blk = nmine > 0 ? i0 % a.nblk : 0;
+  bool need_plan = true;
 #pragma unroll 1
   for (int k = 0; k < nmine; ++k) {
-    const int it = i0 + k;
-    const int tile = it / a.nblk, blk = it % a.nblk;
     if (tile != cur_tile) {
       flush(cur_tile);
       cur_tile = tile;
+      need_plan = true;
     }
     const int s = k % S;
     mbar_wait(&mybar[s], uint32_t((k / S) & 1));
+#ifdef CCQ_GEMV_TRACE
+    if (k == 0) { MTRACE(4, gtime()); }
+#endif
     const uint8_t* st = ring + s * STAGE;
     if constexpr (FAM == kF206) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = g + 8 * h;
-        const uint4 pv = *reinterpret_cast<const uint4*>(st + CODE_B + r * 32 + 16);
-        rc[h].C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
-        rc[h].M = pv.z;
-        const uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
-        rc[h].sel[0] = base;
-        rc[h].sel[1] = base + step;
-        rc[h].sel[2] = base + 2 * step;
-        rc[h].sel[3] = base + 3 * step;
-        rc[h].nib = *reinterpret_cast<const uint32_t*>(st + CODE_B + r * 32 + (blk & 3) * 4);
+        if (need_plan) {  // the row plans change only with the tile
+          const uint4 pv = *reinterpret_cast<const uint4*>(st + CODE_B + r * 32 + 16);
+          rc[h].C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
+          rc[h].M = pv.z;
+          uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
+          if constexpr (P2) {
+            // derive the plan one byte lower: same M, C >> 8, byte position - 1
+            // (exact: floor(floor(v / 2^8) / 2^32) == floor(v / 2^40))
+            rc[h].C >>= 8;
+            step = step > 1u ? step >> 4 : 1u;
+            const uint32_t pos = step == 1u ? 0u : step == 16u ? 1u : step == 256u ? 2u : 3u;
+            base = (0x4444u & ~(0xFu << (4u * pos))) & 0xFFFFu;
+          }
+          rc[h].sel[0] = base;
+          rc[h].sel[1] = base + step;
+          rc[h].sel[2] = base + 2 * step;
+          rc[h].sel[3] = base + 3 * step;
+        }
+        // nibbles of this block's 4 groups: 2 bytes at (blk % 8) * 2
+        rc[h].nib = uint32_t(*reinterpret_cast<const uint16_t*>(st + CODE_B + r * 32 + (blk & 7) * 2));
       }
+      need_plan = false;
     }
-    const int G0 = blk * kBlkG;
-    const int ng = gpr - G0 < kBlkG ? gpr - G0 : kBlkG;
-#pragma unroll 2
-    for (int j = 0; j < ng; ++j) {
-      const int G = G0 + j;
-      uint32_t ua[8], ub[8];
-      const uint32_t sca = decode_units<FAM>(st, g, j, c, rc[0], ua);
-      const uint32_t scb = decode_units<FAM>(st, g + 8, j, c, rc[1], ub);
-      float d[NT][4];
+    const int G0 = blk * F::BLK;
+    if (gpr - G0 >= F::BLK) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int nq = nt * 8 + 2 * c;
-        const float2 q2 = *reinterpret_cast<const float2*>(qs + G * MP + nq);
-        d[nt][0] = -q2.x; d[nt][1] = -q2.y; d[nt][2] = -q2.x; d[nt][3] = -q2.y;
-        const int nb = nt * 8 + g;
-        uint4 b01 = make_uint4(0, 0, 0, 0), b23 = make_uint4(0, 0, 0, 0);
-        if (nb < M) {
-          const uint4* src = reinterpret_cast<const uint4*>(xs + ((size_t(G) * M + nb) * 4 + c) * 32);
-          b01 = src[0];
-          b23 = src[1];
-        }
-        const uint32_t bb[8] = {b01.x, b01.y, b01.z, b01.w, b23.x, b23.y, b23.z, b23.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const uint32_t af[4] = {ua[2 * t], ub[2 * t], ua[2 * t + 1], ub[2 * t + 1]};
-          mma16816(d[nt], af, bb[2 * t], bb[2 * t + 1]);
-        }
-      }
-      const float fa = float(sca), fb = float(scb);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        yacc[nt][0] = fmaf(fa, d[nt][0], yacc[nt][0]);
-        yacc[nt][1] = fmaf(fa, d[nt][1], yacc[nt][1]);
-        yacc[nt][2] = fmaf(fb, d[nt][2], yacc[nt][2]);
-        yacc[nt][3] = fmaf(fb, d[nt][3], yacc[nt][3]);
-      }
+      for (int j = 0; j < F::BLK; ++j) group(st, j, G0 + j);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < gpr - G0; ++j) group(st, j, G0 + j);
     }
     // release the stage and refill it with item k + S
     __syncwarp();
@@ -483,8 +610,15 @@ __global__ void __launch_bounds__(384, 1)
       fence_proxy_async_smem();
       issue(k + S);
     }
+    if (++blk == a.nblk) {
+      blk = 0;
+      ++tile;
+    }
   }
   if (nmine > 0) flush(cur_tile);
+#ifdef CCQ_GEMV_TRACE
+  MTRACE(5, gtime());
+#endif
   __syncthreads();
 
   // ---- per-tile sums in warp order, scaled by super and the token scale ----
@@ -492,16 +626,12 @@ __global__ void __launch_bounds__(384, 1)
   for (int e = threadIdx.x; e < ntl * kRowsT * M; e += blockDim.x) {
     const int tl = e / (kRowsT * M), rem = e % (kRowsT * M);
     const int r = rem / M, n = rem % M;
-    const int tile = t_begin + tl;
-    const int64_t row = int64_t(tile) * kRowsT + r;
+    const int64_t row = int64_t(t_begin + tl) * kRowsT + r;
     if (row >= a.rows) continue;
     float v = 0.f;
     for (int w = 0; w < nw; ++w) {
-      const int wi0 = int(int64_t(w) * nitems / nw), wi1 = int(int64_t(w + 1) * nitems / nw);
-      if (wi1 <= wi0) continue;
-      const int ft = t_begin + wi0 / a.nblk, lt = t_begin + (wi1 - 1) / a.nblk;
-      if (tile < ft || tile > lt) continue;
-      v += part[((size_t(w) * a.slots + (tile - ft)) * kRowsT + r) * MP + n];
+      const int ft = wrange[2 * w], lt = wrange[2 * w + 1];
+      if (tl >= ft && tl <= lt) v += part[((size_t(w) * a.slots + (tl - ft)) * kRowsT + r) * MP + n];
     }
     v *= a.super[row] * tokscale[n];
     if (a.y_dtype == CCQ_DTYPE_F32)
@@ -509,6 +639,9 @@ __global__ void __launch_bounds__(384, 1)
     else
       static_cast<__nv_bfloat16*>(a.y)[int64_t(n) * a.y_ld + row] = __float2bfloat16_rn(v);
   }
+#ifdef CCQ_GEMV_TRACE
+  MTRACE(6, gtime());
+#endif
 }
 
 struct Cfg {
@@ -520,22 +653,23 @@ template <int FAM, int NT, int S>
 Cfg plan_cfg(const ccq_dev_model* m, int M, int grid, int max_smem) {
   using F = MF<FAM>;
   constexpr int MP = 8 * NT;
-  constexpr int STAGE = ((kRowsT * F::BOX + kRowsT * F::SIDE) + 1023) & ~1023;
+  constexpr int STAGE = ((kRowsT * F::BOX + kRowsT * F::SIDE) + 511) & ~511;
   const int ntiles = int((m->rows + kRowsT - 1) / kRowsT);
-  const int nblk = int((m->gpr + kBlkG - 1) / kBlkG);
+  const int nblk = int((m->gpr + F::BLK - 1) / F::BLK);
   const int tiles_cta = (ntiles + grid - 1) / grid;
-  for (int warps = 12; warps >= 4; warps -= 4) {
+  static const int env_w = std::getenv("CCQ_MMA_WARPS") ? std::atoi(std::getenv("CCQ_MMA_WARPS")) : 0;
+  for (int warps = env_w ? env_w : 16; warps >= 4; warps -= 4) {
     const int items = tiles_cta * nblk;
     const int per_warp = (items + warps - 1) / warps;
     const int slots = per_warp / nblk + 2;
-    const size_t smem = size_t(warps) * S * STAGE + size_t(m->gpr) * M * 128 + size_t(m->gpr) * MP * 4 +
-                        size_t(warps) * slots * kRowsT * MP * 4 + MP * 8 + 16 + size_t(warps) * S * 8 + 1024 + 64;
+    const size_t smem = size_t(warps) * S * STAGE + size_t(m->gpr * 128 + 16) * M + size_t(m->gpr) * MP * 4 +
+                        size_t(warps) * slots * kRowsT * MP * 4 + MP * 8 + 256 + size_t(warps) * S * 8 + 8 + 1024 + 64;
     if (smem <= size_t(max_smem)) return Cfg{warps, slots, smem};
   }
   return Cfg{0, 0, 0};
 }
 
-template <int FAM, int NT, int S, int XDT>
+template <int FAM, int NT, int S, int XDT, bool P2>
 int launch_chunk(const ccq_dev_model* m, const CUtensorMap& tmc, const CUtensorMap& tms, const void* x,
                  int M, void* y, int x_dtype, int y_dtype, int grid, const Cfg& cfg, cudaStream_t s) {
   MmaArgs a{};
@@ -549,15 +683,15 @@ int launch_chunk(const ccq_dev_model* m, const CUtensorMap& tmc, const CUtensorM
   a.rows = m->rows;
   a.rows_pad = m->rows_pad;
   a.gpr = m->gpr;
-  a.nblk = int((m->gpr + kBlkG - 1) / kBlkG);
+  a.nblk = int((m->gpr + MF<FAM>::BLK - 1) / MF<FAM>::BLK);
   a.ntiles = int((m->rows + kRowsT - 1) / kRowsT);
   a.slots = cfg.slots;
   a.x_ld = m->cols;
   a.y_ld = m->rows;
-  a.xs_bytes = uint32_t(m->gpr * M * 128);
-  auto kern = gemv_mma<FAM, NT, S, XDT>;
-  static size_t configured[3][3] = {};
-  size_t& conf = configured[NT][XDT];
+  a.xs_bytes = uint32_t((m->gpr * 128 + 16) * M);
+  auto kern = gemv_mma<FAM, NT, S, XDT, P2>;
+  static size_t configured[3][3][2] = {};
+  size_t& conf = configured[NT][XDT][P2 ? 1 : 0];
   if (conf < cfg.smem) {
     CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)));
     conf = cfg.smem;
@@ -578,7 +712,7 @@ int launch_chunk(const ccq_dev_model* m, const CUtensorMap& tmc, const CUtensorM
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemv_mma launch");
 }
 
-template <int FAM>
+template <int FAM, bool P2>
 int launch_fam_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                    cudaStream_t s) {
   using F = MF<FAM>;
@@ -586,7 +720,7 @@ int launch_fam_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
   CUtensorMap tmc{}, tms{};
   int st = make_map_2d(&tmc, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes, m->rec, uint64_t(m->nch) * m->rows_pad,
                        m->rec, F::BOX, kRowsT,
-                       FAM == kF206 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+                       FAM == kF206 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != CCQ_OK) return st;
   if constexpr (F::SIDE > 0) {
     st = make_map_2d(&tms, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes + m->cgb, F::SIDE,
@@ -615,15 +749,13 @@ int launch_fam_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
     void* yc = static_cast<uint8_t*>(y) + size_t(m0) * m->rows * yb;
     if (chunk > 8) {
       switch (x_dtype) {
-        case CCQ_DTYPE_F32: st = launch_chunk<FAM, 2, S, CCQ_DTYPE_F32>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s); break;
-        case CCQ_DTYPE_BF16: st = launch_chunk<FAM, 2, S, CCQ_DTYPE_BF16>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s); break;
-        default: st = launch_chunk<FAM, 2, S, CCQ_DTYPE_F16>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s);
+        case CCQ_DTYPE_BF16: st = launch_chunk<FAM, 2, S, CCQ_DTYPE_BF16, P2>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s); break;
+        default: st = launch_chunk<FAM, 2, S, CCQ_DTYPE_F16, P2>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s);
       }
     } else {
       switch (x_dtype) {
-        case CCQ_DTYPE_F32: st = launch_chunk<FAM, 1, S, CCQ_DTYPE_F32>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s); break;
-        case CCQ_DTYPE_BF16: st = launch_chunk<FAM, 1, S, CCQ_DTYPE_BF16>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s); break;
-        default: st = launch_chunk<FAM, 1, S, CCQ_DTYPE_F16>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s);
+        case CCQ_DTYPE_BF16: st = launch_chunk<FAM, 1, S, CCQ_DTYPE_BF16, P2>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s); break;
+        default: st = launch_chunk<FAM, 1, S, CCQ_DTYPE_F16, P2>(m, tmc, tms, xc, chunk, yc, x_dtype, y_dtype, grid, cfg, s);
       }
     }
     if (st != CCQ_OK) return st;
@@ -634,8 +766,14 @@ int launch_fam_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
 
 }  // namespace
 
+int mma_min_tokens() {
+  const char* e = std::getenv("CCQ_FORCE_MMA");
+  return (e && e[0] == '1') ? 1 : kMmaMinTokens;
+}
+
 bool gemv_mma_supported(const ccq_dev_model* m, int64_t M) {
   (void)M;
+  // activations arrive by 16-byte bulk copies: need 16-B aligned rows
   if (m->geo.group_size != 64 || m->cols % 64 != 0 || m->cols == 0) return false;
   if (std::getenv("CCQ_GEMV_STREAM")) return false;  // debug: force the CUDA-core kernel
   return true;
@@ -643,11 +781,22 @@ bool gemv_mma_supported(const ccq_dev_model* m, int64_t M) {
 
 int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                     cudaStream_t s) {
+  if (x_dtype == CCQ_DTYPE_F32 || (reinterpret_cast<uintptr_t>(x) & 15u))
+    return fail(CCQ_ERR_CONFIG, "gemv_mma needs 16-byte aligned bf16/f16 activations");
   switch (m->family) {
-    case kF275: return launch_fam_mma<kF275>(m, x, x_dtype, M, y, y_dtype, s);
-    case kF25: return launch_fam_mma<kF25>(m, x, x_dtype, M, y, y_dtype, s);
-    default: return launch_fam_mma<kF206>(m, x, x_dtype, M, y, y_dtype, s);
+    case kF275: return launch_fam_mma<kF275, false>(m, x, x_dtype, M, y, y_dtype, s);
+    case kF25: return launch_fam_mma<kF25, false>(m, x, x_dtype, M, y, y_dtype, s);
+    default:
+      return m->plan_pos_min >= 1 ? launch_fam_mma<kF206, true>(m, x, x_dtype, M, y, y_dtype, s)
+                                  : launch_fam_mma<kF206, false>(m, x, x_dtype, M, y, y_dtype, s);
   }
 }
 
 }  // namespace ccqb
+
+#ifdef CCQ_GEMV_TRACE
+extern "C" int ccq_trace_dump_mma(unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, ccqb::g_mtrace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif

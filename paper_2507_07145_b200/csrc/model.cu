@@ -260,6 +260,8 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
     for (int64_t r = 0; r < rp; ++r)
       for (int c = 0; c < m->nch; ++c)
         std::memcpy(rec_at(c, r) + m->cgb + 16, &plans[r], sizeof(WidenPlan));
+    m->plan_pos_min = 3;
+    for (int64_t r = 0; r < rows; ++r) m->plan_pos_min = std::min(m->plan_pos_min, int(plan_pos(plans[r])));
   }
 
   int prev = 0;
@@ -366,8 +368,10 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   if (st != CCQ_OK || M == 0 || m->rows == 0) return st;
   // Dispatch by batch: the tensor-pipe GEMV streams the weights once for up
   // to kMmaMaxTokens tokens; beyond that the tcgen05 GEMM (2.06) takes over.
-  const bool mma = x_dtype != CCQ_DTYPE_F32 && gemv_mma_supported(m, M);
-  if (mma && (M <= kMmaMaxTokens || !gemm_supported(m, M)))
+  const bool mma = x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
+                   gemv_mma_supported(m, M);
+  // (M = 1 on the CUDA-core streaming kernel: measured faster, profiles/r01_*)
+  if (mma && M >= mma_min_tokens() && (M <= kMmaMaxTokens || !gemm_supported(m, M)))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
   if (!gemv_fast_supported(m, M) && gemm_supported(m, M))
     return launch_gemm(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));

@@ -147,9 +147,11 @@ def test_gemv_bf16_device(models, oracle, ccq, cuda, fam, M):
 @pytest.mark.parametrize("fam", [0, 1, 2])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("M", [1, 3, 8, 9, 16, 21])
-def test_gemv_tensor_pipe_bf16_all_shapes(models, oracle, ccq, cuda, fam, shape, M):
+def test_gemv_tensor_pipe_bf16_all_shapes(models, oracle, ccq, cuda, fam, shape, M, monkeypatch):
     """The mma.sync GEMV (bf16 activations): every family, ragged rows/cols,
-    token counts across the n8 / n16 tiles and the 16-token launch chunks."""
+    token counts across the n8 / n16 tiles and the 16-token launch chunks
+    (CCQ_FORCE_MMA routes M = 1 to it as well)."""
+    monkeypatch.setenv("CCQ_FORCE_MMA", "1")
     torch = cuda
     s, d = models[(fam, *shape)]
     x = bf16_round(oracle.random_matrix(M, shape[1], "gaussian", 31 + M))
@@ -163,9 +165,10 @@ def test_gemv_tensor_pipe_bf16_all_shapes(models, oracle, ccq, cuda, fam, shape,
 
 @pytest.mark.parametrize("fam", [0, 1, 2])
 @pytest.mark.parametrize("scale", [1e-30, 1e-6, 1.0, 3e4, 1e30])
-def test_gemv_tensor_pipe_activation_range(models, oracle, ccq, cuda, fam, scale):
+def test_gemv_tensor_pipe_activation_range(models, oracle, ccq, cuda, fam, scale, monkeypatch):
     """Per-token power-of-two rescaling keeps f16 operands exact across the
     whole bf16 range; tokens of very different magnitude share one launch."""
+    monkeypatch.setenv("CCQ_FORCE_MMA", "1")
     torch = cuda
     s, d = models[(fam, 257, 4096)]
     x = oracle.random_matrix(3, 4096, "gaussian", 5)
