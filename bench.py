@@ -274,9 +274,11 @@ def main():
         e2e_ms = float(t.item())
     e2e_val = bytes_step * world / (e2e_ms * 1e-3) / 1e9
 
-    sweep = None
+    sweep = prefill = None
+    tflops_peak = float(peaks.get("bf16_tflops", 1590.0))
     if args.sweep and rank == 0:
-        sweep = run_sweep(P, torch, dev, stream, hbm_peak)
+        sweep = run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak)
+        prefill = run_prefill(P, torch, dev, stream, tflops_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -322,29 +324,36 @@ def main():
             out["cpu_baseline"] = cpu
         if sweep is not None:
             out["sweep"] = sweep
+        if prefill is not None:
+            out["prefill"] = prefill
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 
 
-def run_sweep(P, torch, dev, stream, hbm_peak):
-    """Packed GB/s and TFLOP/s per (family, shape, M) - graph-timed, L2-cold."""
+def run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak):
+    """Packed GB/s and TFLOP/s per (family, shape, M, kernel) - graph-timed,
+    L2-cold (enough resident copies to exceed L2).  kernel "auto" is the
+    dispatcher; "gemv" / "gemm" force a path to show the crossover."""
     from paper_2507_07145_b200.synthetic import random_packed as _synthetic
     res = []
     shapes = [(4096, 14336), (14336, 4096), (4096, 4096)]
+    cases = [(M, "auto") for M in (1, 2, 4, 8, 16, 32, 64, 128, 256)] + \
+            [(M, k) for M in (16, 32, 64) for k in ("gemv", "gemm")]
     for fam, fname in ((2, "2.06"), (1, "2.5"), (0, "2.75")):
         for (din, dout) in shapes:
             copies = max(2, int(160e6 // (din * dout * 0.35)) + 1)
             ms_ = [P.DeviceModel.upload(_synthetic(dout, din, fam, 64, 17 + c), device=dev.index)
                    for c in range(copies)]
             pb = ms_[0].payload_bytes
-            for M in (1, 2, 4, 8, 16):
+            for M, kern in cases:
                 x = torch.randn(M, din, device=dev).to(torch.bfloat16)
                 y = torch.empty(M, dout, device=dev)
+
                 def body():
                     for mm in ms_:
-                        P.matmul(mm, x, out=y, stream=stream)
+                        P.matmul(mm, x, out=y, stream=stream, kernel=kern)
                 with torch.cuda.stream(stream):
                     body()
                 stream.synchronize()
@@ -355,7 +364,7 @@ def run_sweep(P, torch, dev, stream, hbm_peak):
                     g.replay()
                 torch.cuda.synchronize()
                 s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                reps = 20
+                reps = 10
                 with torch.cuda.stream(stream):
                     s0.record(stream)
                     for _ in range(reps):
@@ -363,12 +372,42 @@ def run_sweep(P, torch, dev, stream, hbm_peak):
                     s1.record(stream)
                 torch.cuda.synchronize()
                 us = s0.elapsed_time(s1) * 1e3 / (reps * copies)
-                res.append({"family": fname, "d_in": din, "d_out": dout, "M": M,
+                tf = 2 * M * din * dout / us / 1e6
+                res.append({"family": fname, "d_in": din, "d_out": dout, "M": M, "kernel": kern,
                             "us": round(us, 3), "packed_GBps": round(pb / us / 1e3, 1),
                             "hbm_frac": round(pb / us / 1e3 / hbm_peak, 4),
-                            "TFLOPs": round(2 * M * din * dout / us / 1e6, 3)})
+                            "TFLOPs": round(tf, 2), "tensor_frac": round(tf / tflops_peak, 4)})
             del ms_
     return res
+
+
+def run_prefill(P, torch, dev, stream, tflops_peak):
+    """BASELINE configs[4] on one GPU: 8192 -> 28672, 2.06, M = 4096 (tcgen05 GEMM)."""
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    out = []
+    for fam, fname in ((2, "2.06"), (1, "2.5"), (0, "2.75")):
+        m = P.DeviceModel.upload(_synthetic(28672, 8192, fam, 64, 5), device=dev.index)
+        x = torch.randn(4096, 8192, device=dev).to(torch.bfloat16)
+        y = torch.empty(4096, 28672, device=dev, dtype=torch.bfloat16)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                P.matmul(m, x, out=y, stream=stream)
+        stream.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        with torch.cuda.stream(stream):
+            s0.record(stream)
+            for _ in range(reps):
+                P.matmul(m, x, out=y, stream=stream)
+            s1.record(stream)
+        torch.cuda.synchronize()
+        ms = s0.elapsed_time(s1) / reps
+        tf = 2 * 4096 * 8192 * 28672 / (ms * 1e-3) / 1e12
+        out.append({"family": fname, "d_in": 8192, "d_out": 28672, "M": 4096, "ms": round(ms, 4),
+                    "TFLOPs": round(tf, 1), "tensor_frac": round(tf / tflops_peak, 4),
+                    "out_dtype": "bf16"})
+        del m, x, y
+    return out
 
 
 if __name__ == "__main__":

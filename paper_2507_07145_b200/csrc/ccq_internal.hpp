@@ -84,6 +84,50 @@ __host__ __device__ __forceinline__ uint32_t widen_hi(uint32_t q, const WidenPla
 
 constexpr int kChunk = 32;  // groups per K-chunk in the device layout
 
+// Activation order of the tensor-core kernels for the 2.75 / 2.5 families
+// (gemv_mma.cu, gemm_sm100.cu): 32 f16x2 "units" per 64-weight group, unit
+// U = 8c + u; // (weight index within the group, field power p) of element e (0 = low half,
+// 1 = high half) of unit u (0..7) produced by lane c (0..3).
+struct WP {
+  int w, p;
+};
+__host__ __device__ constexpr WP unit_wp(int fam, int c, int u, int e) {
+  if (fam == kF206) {
+    // natural order: unit u of lane c holds weights 16c + 2u + e (p-free magic)
+    return WP{16 * c + 2 * u + e, 0};
+  }
+  if (fam == kF275) {
+    // bytes B = 5c..5c+4; byte B: shift 4 -> 3B, shift 2 -> 3B+1, shift 0 -> 3B+2
+    const int B0 = 5 * c;
+    if (u < 6) {
+      const int B = B0 + (u / 3) * 2 + e;
+      const int f = u % 3;  // 0: shift 0 (p0), 1: shift 2 (p2), 2: shift 4 (p4)
+      return f == 0 ? WP{3 * B + 2, 0} : f == 1 ? WP{3 * B + 1, 2} : WP{3 * B, 4};
+    }
+    const int B4 = B0 + 4;
+    if (u == 6) {
+      if (e == 0) return WP{3 * B4, 4};
+      // extra weight: b20 shift 4 / 2 / 0 for lanes 0..2, tail state (b21 >> 4) for lane 3
+      return c == 0 ? WP{60, 4} : c == 1 ? WP{61, 2} : c == 2 ? WP{62, 0} : WP{63, 4};
+    }
+    return e == 0 ? WP{3 * B4 + 1, 2} : WP{3 * B4 + 2, 0};
+  }
+  // 2.5: words W = 2c (low half), 2c+1 (high half); field k of word w is
+  // weight 7w + k with shifts [13,11,9,6,4,2,0]
+  if (u < 7) {
+    const int w = 2 * c + e;
+    // u: 0 sh0 p0, 1 sh2 p2, 2 sh4 p4, 3 sh6 p6, 4 sh9 p0, 5 sh11 p2, 6 sh13 p4
+    const int k = u == 0 ? 6 : u == 1 ? 5 : u == 2 ? 4 : u == 3 ? 3 : u == 4 ? 2 : u == 5 ? 1 : 0;
+    const int p = u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 4 : u == 3 ? 6 : u == 4 ? 0 : u == 5 ? 2 : 4;
+    return WP{7 * w + k, p};
+  }
+  // unit 7 from words 8 (and 9)
+  if (c == 0) return e == 0 ? WP{56 + 6, 0} : WP{56 + 5, 2};
+  if (c == 1) return e == 0 ? WP{56 + 4, 4} : WP{56 + 3, 6};
+  if (c == 2) return e == 0 ? WP{56 + 2, 1} : WP{56 + 1, 3};
+  return e == 0 ? WP{56 + 0, 5} : WP{63, 5};
+}
+
 // Read-only view of the device layout, passed to kernels by value.
 struct DevLayout {
   const uint8_t* codes;  // record base
@@ -169,6 +213,7 @@ constexpr int kMmaMinTokens = 2;  // M = 1: CUDA-core streaming GEMV (gemv.cu)
 bool gemv_mma_supported(const ccq_dev_model* m, int64_t M);
 // smallest batch routed to the tensor-pipe GEMV (env CCQ_FORCE_MMA=1 -> 1, for tests)
 int mma_min_tokens();
+bool gemv_mma_fits(const ccq_dev_model* m, int64_t M);
 int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                     int y_dtype, cudaStream_t s);
 int num_sms(int device);

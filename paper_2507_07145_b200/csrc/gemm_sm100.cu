@@ -146,6 +146,34 @@ __global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __h
   sh = sh > 126 ? 126 : (sh < -126 ? -126 : sh);
   const float scale = __int_as_float((127 + sh) << 23);
   if (threadIdx.x == 0) inv_scale[m] = __int_as_float((127 - sh) << 23);
+  if constexpr (FAM != kF206) {
+    // 2.75 / 2.5: K position 2U + e of a group holds weight unit_wp(c, u, e)
+    // (U = 8c + u) scaled by 2^-p - the order the GEMM decoders emit
+    for (int64_t q = threadIdx.x; q < K / 2; q += blockDim.x) {
+      const int64_t G = q / 32;
+      const int U = int(q % 32), cc = U / 8, u = U % 8;
+      const WP w0 = unit_wp(FAM, cc, u, 0), w1 = unit_wp(FAM, cc, u, 1);
+      float v0, v1;
+      if constexpr (XDT == CCQ_DTYPE_F32) {
+        v0 = static_cast<const float*>(x)[m * K + G * 64 + w0.w];
+        v1 = static_cast<const float*>(x)[m * K + G * 64 + w1.w];
+      } else {
+        const uint16_t h0 = static_cast<const uint16_t*>(x)[m * K + G * 64 + w0.w];
+        const uint16_t h1 = static_cast<const uint16_t*>(x)[m * K + G * 64 + w1.w];
+        v0 = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(uint32_t(h0) << 16) : __half2float(__ushort_as_half(h0));
+        v1 = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(uint32_t(h1) << 16) : __half2float(__ushort_as_half(h1));
+      }
+      const float t0 = v0 * scale * __int_as_float((127 - w0.p) << 23);
+      const float t1 = v1 * scale * __int_as_float((127 - w1.p) << 23);
+      const __half2 hv = __floats2half2_rn(t0, t1);
+      *reinterpret_cast<__half2*>(out + (m * XS) * K + 2 * q) = hv;
+      if constexpr (XS == 2) {
+        const float2 f = __half22float2(hv);
+        *reinterpret_cast<__half2*>(out + (m * XS + 1) * K + 2 * q) = __floats2half2_rn(t0 - f.x, t1 - f.y);
+      }
+    }
+    return;
+  }
   for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
     const int64_t k0 = q * 4;
     float v[4];
@@ -226,27 +254,50 @@ __device__ __forceinline__ uint32_t hfma2_u32(uint32_t a, uint32_t b, uint32_t c
 // the MMA issuing thread costs ~200 cycles (measured, tools/micro/mma_loop.cu)
 // while 4 MMAs of N = 64 take ~180, so small-N tiles batch several groups per
 // wait; at N = 256 one group (512 MMA cycles) already hides it.
-template <int BN>
-constexpr int groups_per_stage() { return BN <= 64 ? 4 : (BN <= 128 ? 2 : 1); }
+// Family traits of the GEMM: code box bytes per row (8 groups), code ring
+// depth, side-band nibbles, and SPLIT = number of f16 operand parts per
+// weight (2.5: 13-bit scales do not fit f16 exactly; sc = 64 hi + lo gives
+// two exact operands and two accumulators, combined in the epilogue).
+template <int FAM>
+struct GF;
+template <>
+struct GF<kF206> {
+  static constexpr int BOXB = 128, STAGES_C = 5, NIB = 1, SPLIT = 1;
+};
+template <>
+struct GF<kF275> {
+  static constexpr int BOXB = 176, STAGES_C = 4, NIB = 0, SPLIT = 1;
+};
+template <>
+struct GF<kF25> {
+  static constexpr int BOXB = 160, STAGES_C = 4, NIB = 0, SPLIT = 2;
+};
+
+template <int FAM, int BN>
+constexpr int groups_per_stage() {
+  return GF<FAM>::SPLIT == 2 ? (BN <= 64 ? 2 : 1) : (BN <= 64 ? 4 : (BN <= 128 ? 2 : 1));
+}
 template <int BN>
 constexpr int stages_a() { return BN <= 64 ? 3 : 4; }
-template <int BN>
-constexpr int stages_b() { return stages_a<BN>(); }
 
-template <int BN>
+template <int FAM, int BN>
 struct GemmSmem {
   static constexpr int SA = stages_a<BN>();
-  static constexpr int SB = stages_b<BN>();
-  static constexpr int G = groups_per_stage<BN>();
+  static constexpr int SB = SA;
+  static constexpr int G = groups_per_stage<FAM, BN>();
+  static constexpr int SC = GF<FAM>::STAGES_C;
   static constexpr int B_BLOCK = BN * kBK * 2;               // BN x 128 B per group
   static constexpr int B_BYTES = G * B_BLOCK;
-  static constexpr int C_BYTES = kBM * kCodeBox;             // 16 KB codes
-  static constexpr int N_BYTES = kBM * 16;                   // 2 KB nibbles
+  static constexpr int C_BYTES = kBM * GF<FAM>::BOXB;        // 128 rows x 8 groups of codes
+  static constexpr int N_BYTES = GF<FAM>::NIB ? kBM * 16 : 0;  // side-band nibbles (2.06)
   static constexpr int OFF_B = 0;                            // 1024-aligned
   static constexpr int OFF_C = OFF_B + SB * B_BYTES;
-  static constexpr int OFF_N = OFF_C + kStagesC * C_BYTES;
-  static constexpr int OFF_BAR = OFF_N + kStagesC * N_BYTES;
+  static constexpr int OFF_N = OFF_C + SC * C_BYTES;
+  static constexpr int OFF_BAR = OFF_N + SC * N_BYTES;
   static constexpr int TOTAL = OFF_BAR + 512 + 1024;  // + alignment slack
+  static constexpr int TMEM_NEED = GF<FAM>::SPLIT * BN + SA * G * GF<FAM>::SPLIT * kACols;
+  static_assert(TMEM_NEED <= 512, "TMEM budget");
+  static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ void store_y(const GemmArgs& a, int64_t idx, float out) {
@@ -256,12 +307,118 @@ __device__ __forceinline__ void store_y(const GemmArgs& a, int64_t idx, float ou
     static_cast<__nv_bfloat16*>(a.y)[idx] = __float2bfloat16_rn(out);
 }
 
-template <int BN>
+
+// f16 bit pattern of a small non-negative integer (exact below 2048).
+__host__ __device__ constexpr uint32_t f16_int(int v) {
+  if (v == 0) return 0u;
+  int e = 0;
+  while ((2 << e) <= v) ++e;
+  return uint32_t(((e + 15) << 10) | ((v << (10 - e)) & 0x3FF));
+}
+__host__ __device__ constexpr uint32_t f16x2_int(int lo, int hi) { return f16_int(lo) | (f16_int(hi) << 16); }
+
+__device__ __forceinline__ uint32_t lop_m(uint32_t v, uint32_t mask) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(v), "r"(mask), "r"(0x64006400u));
+  return d;
+}
+__device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// 2.75: one 22-byte group (row base rb, group j of the 8-group code box) ->
+// 32 f16x2 columns sc*(s-8)*2^p in the unit order of unit_wp (ccq_internal.hpp).
+__device__ __forceinline__ void decode_gemm_275(const uint8_t* rb, int j, uint32_t (&h)[32]) {
+  const int off = 22 * j;
+  const uint32_t* gp = reinterpret_cast<const uint32_t*>(rb + (off & ~3));
+  const uint32_t sh = 8u * uint32_t(off & 3);
+  uint32_t w[7];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) w[i] = gp[i];
+  uint32_t B[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) B[i] = __funnelshift_r(w[i], w[i + 1], sh);
+  const uint32_t sc = (B[5] >> 8) & 0xFu;  // tail byte 21, low nibble
+  const float fs = float(sc);
+  const __half2 sc2 = __float2half2_rn(fs);
+  const uint32_t scu = *reinterpret_cast<const uint32_t*>(&sc2);
+  // bias -(1024 + 8*2^p) * sc, exact in f16 for sc <= 15
+  auto bias = [&](int plo, int phi) {
+    const __half2 b = __floats2half2_rn(-(1024.f + 8.f * float(1 << plo)) * fs, -(1024.f + 8.f * float(1 << phi)) * fs);
+    return *reinterpret_cast<const uint32_t*>(&b);
+  };
+  const uint32_t b00 = bias(0, 0), b22 = bias(2, 2), b44 = bias(4, 4), b42 = bias(4, 2), b40 = bias(4, 0),
+                 b20 = bias(2, 0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int bb = 5 * c;
+    const uint32_t lo = __funnelshift_r(B[bb >> 2], B[(bb >> 2) + 1], 8u * uint32_t(bb & 3));
+    const uint32_t hi = B[(bb + 4) >> 2] >> (8u * uint32_t((bb + 4) & 3));
+    const uint32_t p0 = prmt(lo, 0u, 0x1100u), p1 = prmt(lo, 0u, 0x3322u);
+    h[8 * c + 0] = hfma2_u32(lop_m(p0, 0x000F000Fu), scu, b00);
+    h[8 * c + 1] = hfma2_u32(lop_m(p0, 0x003C003Cu), scu, b22);
+    h[8 * c + 2] = hfma2_u32(lop_m(p0, 0x00F000F0u), scu, b44);
+    h[8 * c + 3] = hfma2_u32(lop_m(p1, 0x000F000Fu), scu, b00);
+    h[8 * c + 4] = hfma2_u32(lop_m(p1, 0x003C003Cu), scu, b22);
+    h[8 * c + 5] = hfma2_u32(lop_m(p1, 0x00F000F0u), scu, b44);
+    const uint32_t eb = 4u + (c == 3 ? 1u : 0u);  // b20 (lanes 0..2) or b21 (lane 3) of B[5]
+    const uint32_t me = c == 0 ? 0xF0u : c == 1 ? 0x3Cu : c == 2 ? 0x0Fu : 0xF0u;
+    h[8 * c + 6] = hfma2_u32(lop_m(prmt(hi, B[5], (eb << 12) | (eb << 8)), 0x000000F0u | (me << 16)), scu,
+                             c == 1 ? b42 : c == 2 ? b40 : b44);
+    h[8 * c + 7] = hfma2_u32(lop_m(prmt(hi, 0u, 0x0000u), 0x000F003Cu), scu, b20);
+  }
+}
+
+// 2.5: one 20-byte group -> 32 f16x2 columns for each of the two exact
+// operand parts: lo*(s-4)*2^p and hi*(s-4)*2^p with sc = 64 hi + lo.
+__device__ __forceinline__ void decode_gemm_25(const uint8_t* gb, uint32_t (&hl)[32], uint32_t (&hh)[32]) {
+  uint32_t W[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) W[i] = reinterpret_cast<const uint32_t*>(gb)[i];
+  const uint32_t sc = (W[4] >> 16) & 0x1FFFu;
+  const __half2 lo2 = __float2half2_rn(float(sc & 63u)), hi2 = __float2half2_rn(float(sc >> 6));
+  const uint32_t lou = *reinterpret_cast<const uint32_t*>(&lo2), hiu = *reinterpret_cast<const uint32_t*>(&hi2);
+  auto put = [&](int idx, uint32_t unit, uint32_t magicz) {
+    const uint32_t t = hsub2_u32(unit, magicz);  // (s - 4) * 2^p, exact
+    hl[idx] = hmul2_u32(t, lou);
+    hh[idx] = hmul2_u32(t, hiu);
+  };
+  constexpr uint32_t z0 = f16x2_int(1028, 1028), z2 = f16x2_int(1040, 1040), z4 = f16x2_int(1088, 1088),
+                     z6 = f16x2_int(1280, 1280);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t v = W[c], sv = v >> 9;
+    put(8 * c + 0, lop_m(v, 0x00070007u), z0);
+    put(8 * c + 1, lop_m(v, 0x001C001Cu), z2);
+    put(8 * c + 2, lop_m(v, 0x00700070u), z4);
+    put(8 * c + 3, lop_m(v, 0x01C001C0u), z6);
+    put(8 * c + 4, lop_m(sv, 0x00070007u), z0);
+    put(8 * c + 5, lop_m(sv, 0x001C001Cu), z2);
+    put(8 * c + 6, lop_m(sv, 0x00700070u), z4);
+    const uint32_t sel = c == 0 ? 0x1010u : c == 1 ? 0x1010u : c == 2 ? 0x1111u : 0x3311u;
+    const uint32_t mk = c == 0 ? 0x001C0007u : c == 1 ? 0x01C00070u : c == 2 ? 0x0038000Eu : 0x00E000E0u;
+    const uint32_t zz = c == 0 ? f16x2_int(1028, 1040) : c == 1 ? f16x2_int(1088, 1280)
+                      : c == 2 ? f16x2_int(1032, 1056) : f16x2_int(1152, 1152);
+    put(8 * c + 7, lop_m(prmt(W[4], W[4], sel), mk), zz);
+  }
+}
+
+template <int FAM, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_206(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
+    gemm_ccq(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
              const __grid_constant__ CUtensorMap tm_x, GemmArgs a) {
-  using SM = GemmSmem<BN>;
+  using SM = GemmSmem<FAM, BN>;
   constexpr int SA = SM::SA, SB = SM::SB, G = SM::G;
+  constexpr int SPLIT = GF<FAM>::SPLIT;
+  constexpr int kStagesC = SM::SC;
+  constexpr int kCodeBox = GF<FAM>::BOXB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
@@ -314,14 +471,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tm_nib);
     prefetch_tmap(&tm_x);
   }
-  constexpr int kTmemNeed = BN + SA * G * kACols;
+  constexpr int kTmemNeed = SM::TMEM_NEED;
   constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   if (warp == kWarpMma) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_d = *tmem_slot;        // accumulator: columns [0, BN)
-  const uint32_t tmem_a = tmem_d + BN;        // A stages: SA x G x kACols columns
+  const uint32_t tmem_d = *tmem_slot;        // accumulator(s): columns [0, SPLIT * BN)
+  const uint32_t tmem_a = tmem_d + SPLIT * BN;  // A stages: SA x G x SPLIT x kACols columns
   const int nst = (nkb + G - 1) / G;          // pipeline stages (G groups each)
 
   if (warp == kWarpB) {
@@ -347,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int c = kb / kChunk, jb = (kb % kChunk) / 8;
         const int y = int(int64_t(c) * a.rows_pad + r0);
         tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES, &tm_codes, jb * kCodeBox, y, &code_full[cs]);
-        tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
+        if constexpr (GF<FAM>::NIB) tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
       }
     }
   } else if (warp == kWarpMma) {
@@ -375,7 +532,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             // A from TMEM (lane = weight row, 8 columns per K = 16);
             // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
             const uint64_t db = smem_desc(b_base + gg * SM::B_BLOCK + k * 32, 16, 1024, 2);
-            mma_f16_ts(tmem_d, tmem_a + (s * G + gg) * kACols + k * 8, db, idesc, (st | gg | k) != 0);
+#pragma unroll
+            for (int h = 0; h < SPLIT; ++h)
+              mma_f16_ts(tmem_d + h * BN, tmem_a + ((s * G + gg) * SPLIT + h) * kACols + k * 8, db, idesc,
+                         (st | gg | k) != 0);
           }
         }
         mma_commit(&empty[s]);
@@ -396,7 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t row = r0 + r;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
     WidenPlan pl = WidenPlan{0, 0, plan_sel(0)};
-    if (row < row_end) pl = a.plan[row];
+    if constexpr (FAM == kF206)
+      if (row < row_end) pl = a.plan[row];
     const uint32_t selb = pl.sel & 0xFFFFu, step = pl.sel >> 16;
     const uint32_t sel[4] = {selb, selb + step, selb + 2 * step, selb + 3 * step};
     uint32_t magic, mask, shift26;
@@ -430,29 +591,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
       mbar_wait(&code_full[cs], (cb / kStagesC) & 1);
       GT(t_code);
-      const int jb = (kb % kChunk) / 8;
-      uint32_t nibword;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
-                   : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4)));
-      const uint4 cw = lds128(cstage + r * kCodeBox + ((j ^ (r & 7)) << 4));
-      const uint32_t sc = (nibword >> (4 * j)) & 0xFu;
-      // half2 (sc, sc) and bias (-(1024+32) sc, -(1024+256) sc), exact in f16
-      const __half2 sc2 = __hsub2(__halves2half2(__ushort_as_half(uint16_t(0x6400u | sc)),
-                                                 __ushort_as_half(uint16_t(0x6400u | sc))),
-                                  __float2half2_rn(1024.f));
-      const __half2 bias2 = __hmul2(sc2, __floats2half2_rn(-1056.f, -1280.f));
-      const uint32_t scu = *reinterpret_cast<const uint32_t*>(&sc2);
-      const uint32_t biasu = *reinterpret_cast<const uint32_t*>(&bias2);
-      const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
       uint32_t h[32];
-#pragma unroll
-      for (int byte = 0; byte < 16; ++byte) {
-        const uint32_t qb = prmt(words[byte >> 2], 0u, sel[byte & 3]);
-        const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);  // code at [8,23)
-        const uint32_t w2 = prmt(hi, 0u, 0x2121u);                        // code | code << 16
-        const uint32_t w3 = __umulhi(w2, shift26);                         // w2 >> 6
-        h[2 * byte] = hfma2_u32(lop_mask_or(w2, mask, magic), scu, biasu);     // (s3, 8 s2)
-        h[2 * byte + 1] = hfma2_u32(lop_mask_or(w3, mask, magic), scu, biasu); // (s1, 8 s0)
+      uint32_t h2[SPLIT == 2 ? 32 : 1];
+      if constexpr (FAM == kF206) {
+        const int jb = (kb % kChunk) / 8;
+        uint32_t nibword;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
+                     : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4)));
+        const uint4 cw = lds128(cstage + r * kCodeBox + ((j ^ (r & 7)) << 4));
+        const uint32_t sc = (nibword >> (4 * j)) & 0xFu;
+        // half2 (sc, sc) and bias (-(1024+32) sc, -(1024+256) sc), exact in f16
+        const __half2 sc2 = __hsub2(__halves2half2(__ushort_as_half(uint16_t(0x6400u | sc)),
+                                                   __ushort_as_half(uint16_t(0x6400u | sc))),
+                                    __float2half2_rn(1024.f));
+        const __half2 bias2 = __hmul2(sc2, __floats2half2_rn(-1056.f, -1280.f));
+        const uint32_t scu = *reinterpret_cast<const uint32_t*>(&sc2);
+        const uint32_t biasu = *reinterpret_cast<const uint32_t*>(&bias2);
+        const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+  #pragma unroll
+        for (int byte = 0; byte < 16; ++byte) {
+          const uint32_t qb = prmt(words[byte >> 2], 0u, sel[byte & 3]);
+          const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);  // code at [8,23)
+          const uint32_t w2 = prmt(hi, 0u, 0x2121u);                        // code | code << 16
+          const uint32_t w3 = __umulhi(w2, shift26);                         // w2 >> 6
+          h[2 * byte] = hfma2_u32(lop_mask_or(w2, mask, magic), scu, biasu);     // (s3, 8 s2)
+          h[2 * byte + 1] = hfma2_u32(lop_mask_or(w3, mask, magic), scu, biasu); // (s1, 8 s0)
+        }
+      } else if constexpr (FAM == kF275) {
+        decode_gemm_275(cstage + r * kCodeBox, j, h);
+      } else {
+        decode_gemm_25(cstage + r * kCodeBox + 20 * j, h, h2);
       }
       GT(t_dec);
       if (gg == 0) {
@@ -460,7 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         GT(t_empty);
         tc_fence_after();
       }
-      tmem_st32(tmem_a + lane_base + (s * G + gg) * kACols, h);
+      tmem_st32(tmem_a + lane_base + ((s * G + gg) * SPLIT) * kACols, h);
+      if constexpr (SPLIT == 2) tmem_st32(tmem_a + lane_base + ((s * G + gg) * SPLIT + 1) * kACols, h2);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -484,6 +653,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int cc = parity * 32; cc < BN; cc += 32 * kPar) {
       uint32_t v[32];
       tmem_ld32(tmem_d + lane_base + cc, v);
+      if constexpr (SPLIT == 2) {
+        uint32_t vh[32];
+        tmem_ld32(tmem_d + BN + lane_base + cc, vh);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(fmaf(64.f, __uint_as_float(vh[i]), __uint_as_float(v[i])));
+      }
       tmem_ld_wait();
       if (row < row_end) {
         if (a.xs == 1) {
@@ -509,11 +685,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpMma) tmem_dealloc<kTmemCols>(tmem_d);
 }
 
-template <int BN>
-int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+template <int FAM, int BN>
+int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
             cudaStream_t s, const int32_t* offsets_dev = nullptr, int64_t rows_e = 0, int E = 0,
             int64_t max_tokens = 0) {
-  using SM = GemmSmem<BN>;
+  using SM = GemmSmem<FAM, BN>;
   const int64_t K = m->cols;
   const bool grouped = offsets_dev != nullptr;
   const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
@@ -524,18 +700,19 @@ int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void*
   if (M > 0) {
     const unsigned blocks = unsigned(M);
     if (x_dtype == CCQ_DTYPE_F32)
-      x_prepass<kF206, CCQ_DTYPE_F32, 2><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
+      x_prepass<FAM, CCQ_DTYPE_F32, 2><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
     else if (x_dtype == CCQ_DTYPE_BF16)
-      x_prepass<kF206, CCQ_DTYPE_BF16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
+      x_prepass<FAM, CCQ_DTYPE_BF16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
     else
-      x_prepass<kF206, CCQ_DTYPE_F16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
+      x_prepass<FAM, CCQ_DTYPE_F16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
     count_launch();
   }
   CUtensorMap tm_codes, tm_nib, tm_x;
   int st = make_map_2d(&tm_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes, m->rec,
-                       uint64_t(m->nch) * m->rows_pad, m->rec, kCodeBox, kBM,
-                       CU_TENSOR_MAP_SWIZZLE_128B);
-  if (st == CCQ_OK)
+                       uint64_t(m->nch) * m->rows_pad, m->rec, GF<FAM>::BOXB, kBM,
+                       FAM == kF206 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st == CCQ_OK && FAM != kF206) tm_nib = tm_codes;
+  if (st == CCQ_OK && FAM == kF206)
     st = make_map_2d(&tm_nib, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes + m->cgb, 16,
                      uint64_t(m->nch) * m->rows_pad, m->rec, 16, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st == CCQ_OK)
@@ -547,7 +724,7 @@ int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void*
   }
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
              offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale};
-  auto kern = gemm_206<BN>;
+  auto kern = gemm_ccq<FAM, BN>;
   static bool configured[5] = {};
   if (!configured[BN / 64]) {
     CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL));
@@ -569,15 +746,25 @@ int run_206(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void*
 
 bool gemm_supported(const ccq_dev_model* m, int64_t M) {
   (void)M;
-  return m->family == kF206 && m->geo.group_size == 64 && m->cols % 64 == 0 && m->cols > 0;
+  return m->geo.group_size == 64 && m->cols % 64 == 0 && m->cols > 0;
 }
 
 int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
   const int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * M : M;  // BN is chosen on activation rows
-  if (xr <= 64) return run_206<64>(m, x, x_dtype, M, y, y_dtype, s);
-  if (xr <= 128) return run_206<128>(m, x, x_dtype, M, y, y_dtype, s);
-  return run_206<256>(m, x, x_dtype, M, y, y_dtype, s);
+  switch (m->family) {
+    case kF275:
+      if (xr <= 64) return run_gemm<kF275, 64>(m, x, x_dtype, M, y, y_dtype, s);
+      if (xr <= 128) return run_gemm<kF275, 128>(m, x, x_dtype, M, y, y_dtype, s);
+      return run_gemm<kF275, 256>(m, x, x_dtype, M, y, y_dtype, s);
+    case kF25:  // two accumulators: at most 128 token columns per tile
+      if (xr <= 64) return run_gemm<kF25, 64>(m, x, x_dtype, M, y, y_dtype, s);
+      return run_gemm<kF25, 128>(m, x, x_dtype, M, y, y_dtype, s);
+    default:
+      if (xr <= 64) return run_gemm<kF206, 64>(m, x, x_dtype, M, y, y_dtype, s);
+      if (xr <= 128) return run_gemm<kF206, 128>(m, x, x_dtype, M, y, y_dtype, s);
+      return run_gemm<kF206, 256>(m, x, x_dtype, M, y, y_dtype, s);
+  }
 }
 
 // Kernel (d): all experts of a stacked model in ONE launch.  T = total tokens
@@ -587,11 +774,21 @@ int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const
                         int y_dtype, cudaStream_t s) {
   if (max_tokens <= 0 || T <= 0) return CCQ_OK;
   const int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * max_tokens : max_tokens;
-  if (xr <= 64)
-    return run_206<64>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens);
-  if (xr <= 128)
-    return run_206<128>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens);
-  return run_206<256>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens);
+#define CCQ_GROUPED(F, B) run_gemm<F, B>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens)
+  switch (stack->family) {
+    case kF275:
+      if (xr <= 64) return CCQ_GROUPED(kF275, 64);
+      if (xr <= 128) return CCQ_GROUPED(kF275, 128);
+      return CCQ_GROUPED(kF275, 256);
+    case kF25:
+      if (xr <= 64) return CCQ_GROUPED(kF25, 64);
+      return CCQ_GROUPED(kF25, 128);
+    default:
+      if (xr <= 64) return CCQ_GROUPED(kF206, 64);
+      if (xr <= 128) return CCQ_GROUPED(kF206, 128);
+      return CCQ_GROUPED(kF206, 256);
+  }
+#undef CCQ_GROUPED
 }
 
 }  // namespace ccqb

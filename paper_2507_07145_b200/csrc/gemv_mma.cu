@@ -70,48 +70,6 @@ struct MF<kF25> {
   static constexpr int PB = 20, ZP = 4, BLK = 4, BOX = 80, SIDE = 0;
 };
 
-// (weight index within the group, field power p) of element e (0 = low half,
-// 1 = high half) of unit u (0..7) produced by lane c (0..3).
-struct WP {
-  int w, p;
-};
-__host__ __device__ constexpr WP unit_wp(int fam, int c, int u, int e) {
-  if (fam == kF206) {
-    // natural order: unit u of lane c holds weights 16c + 2u + e (p-free magic)
-    return WP{16 * c + 2 * u + e, 0};
-  }
-  if (fam == kF275) {
-    // bytes B = 5c..5c+4; byte B: shift 4 -> 3B, shift 2 -> 3B+1, shift 0 -> 3B+2
-    const int B0 = 5 * c;
-    if (u < 6) {
-      const int B = B0 + (u / 3) * 2 + e;
-      const int f = u % 3;  // 0: shift 0 (p0), 1: shift 2 (p2), 2: shift 4 (p4)
-      return f == 0 ? WP{3 * B + 2, 0} : f == 1 ? WP{3 * B + 1, 2} : WP{3 * B, 4};
-    }
-    const int B4 = B0 + 4;
-    if (u == 6) {
-      if (e == 0) return WP{3 * B4, 4};
-      // extra weight: b20 shift 4 / 2 / 0 for lanes 0..2, tail state (b21 >> 4) for lane 3
-      return c == 0 ? WP{60, 4} : c == 1 ? WP{61, 2} : c == 2 ? WP{62, 0} : WP{63, 4};
-    }
-    return e == 0 ? WP{3 * B4 + 1, 2} : WP{3 * B4 + 2, 0};
-  }
-  // 2.5: words W = 2c (low half), 2c+1 (high half); field k of word w is
-  // weight 7w + k with shifts [13,11,9,6,4,2,0]
-  if (u < 7) {
-    const int w = 2 * c + e;
-    // u: 0 sh0 p0, 1 sh2 p2, 2 sh4 p4, 3 sh6 p6, 4 sh9 p0, 5 sh11 p2, 6 sh13 p4
-    const int k = u == 0 ? 6 : u == 1 ? 5 : u == 2 ? 4 : u == 3 ? 3 : u == 4 ? 2 : u == 5 ? 1 : 0;
-    const int p = u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 4 : u == 3 ? 6 : u == 4 ? 0 : u == 5 ? 2 : 4;
-    return WP{7 * w + k, p};
-  }
-  // unit 7 from words 8 (and 9)
-  if (c == 0) return e == 0 ? WP{56 + 6, 0} : WP{56 + 5, 2};
-  if (c == 1) return e == 0 ? WP{56 + 4, 4} : WP{56 + 3, 6};
-  if (c == 2) return e == 0 ? WP{56 + 2, 1} : WP{56 + 1, 3};
-  return e == 0 ? WP{56 + 0, 5} : WP{63, 5};
-}
-
 __device__ __forceinline__ uint32_t lop_or(uint32_t v, uint32_t mask) {
   uint32_t d;
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(v), "r"(mask), "r"(kMagic));
@@ -252,7 +210,149 @@ struct MmaArgs {
   int slots;        // partial slots per warp
   int64_t x_ld, y_ld;  // elements between token rows of x / y
   uint32_t xs_bytes;   // staged activation bytes (gpr * M * 128)
+  // record path (gemv_rec): device records, their stride, K chunks, ring depth
+  const uint8_t* codes;
+  uint32_t rec;
+  int nch;
+  int S;
 };
+
+// Activations -> shared memory in the f16 operand layout of the family (see
+// the kernel comment): per-token power-of-two scale, -Q per (group, token).
+// Called by every thread of the CTA (contains __syncthreads).
+template <int FAM, int MP, int XDT>
+__device__ __forceinline__ void stage_activations(const MmaArgs& a, uint8_t* xs, float* qs, float* tokscale,
+                                                  int* tokmax, int M, int gpr, int lane) {
+  using F = MF<FAM>;
+  // ---- activations: raw rows in by bulk copy, per-token power-of-two scale,
+  //      then converted IN PLACE to f16 (same byte size) ----
+  const uint32_t row_bytes = uint32_t(gpr) * 128u;
+  const uint32_t tok_stride = row_bytes + 16u;  // +16 B: tokens land in different banks
+  auto to_f32 = [](uint32_t wv, float& lo, float& hi) {
+    if constexpr (XDT == CCQ_DTYPE_BF16) {
+      lo = __uint_as_float(wv << 16);
+      hi = __uint_as_float(wv & 0xFFFF0000u);
+    } else {
+      lo = __half2float(__ushort_as_half(uint16_t(wv & 0xFFFFu)));
+      hi = __half2float(__ushort_as_half(uint16_t(wv >> 16)));
+    }
+  };
+  const int chunks = gpr * 8;  // 16-byte chunks per token
+  {
+    // every thread loads 16-byte chunks of x straight from global memory,
+    // keeps a running max per token and parks the raw bytes in xs
+    float mx[MP];
+#pragma unroll
+    for (int n = 0; n < MP; ++n) mx[n] = 0.f;
+    for (int idx = threadIdx.x; idx < chunks * M; idx += blockDim.x) {
+      const int n = idx / chunks, i = idx - n * chunks;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + int64_t(n) * a.x_ld) + i);
+      *reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16) = v;
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      float m = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float lo, hi;
+        to_f32(wv[q], lo, hi);
+        m = fmaxf(m, fmaxf(fabsf(lo), fabsf(hi)));
+      }
+#pragma unroll
+      for (int nn = 0; nn < MP; ++nn)
+        if (nn == n) mx[nn] = fmaxf(mx[nn], m);
+    }
+#pragma unroll
+    for (int n = 0; n < MP; ++n) {
+      if (n >= M) break;
+      float m = mx[n];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0 && m > 0.f) atomicMax(&tokmax[n], __float_as_int(fminf(m, 3.0e38f)));
+    }
+  }
+  __syncthreads();
+  auto token_scale = [&](int n) {
+    const float mxv = __int_as_float(tokmax[n]);
+    int ex = 0;
+    if (mxv > 0.f) frexpf(mxv, &ex);
+    int sh = mxv > 0.f ? 15 - ex : 0;
+    return sh > 100 ? 100 : (sh < -100 ? -100 : sh);
+  };
+  if constexpr (FAM == kF206) {
+    // natural K order: one 16-byte chunk (8 weights) per thread, in place;
+    // Q of a group = 8 consecutive chunks, combined by shuffles.
+    // Q coefficients: offset (128 for even, 1024 for odd weights) + zero point
+    for (int job0 = threadIdx.x - lane; job0 < chunks * M; job0 += blockDim.x) {
+      const int idx = job0 + lane;
+      const bool live = idx < chunks * M;
+      const int n = live ? idx / chunks : 0, i = live ? idx % chunks : 0;
+      uint4* ptr = reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16);
+      float qpart = 0.f;
+      if (live) {
+        const int sh = token_scale(n);
+        const float scale = ldexpf(1.f, sh);
+        if (i == 0) tokscale[n] = ldexpf(1.f, -sh);
+        const uint4 v = *ptr;
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float lo, hi;
+          to_f32(wv[q], lo, hi);
+          const __half2 h = __floats2half2_rn(lo * scale, hi * scale);
+          const float2 hf = __half22float2(h);
+          qpart = fmaf(128.f + float(F::ZP), hf.x, qpart);
+          qpart = fmaf(1024.f + float(F::ZP), hf.y, qpart);
+          o[q] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        *ptr = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      qpart += __shfl_xor_sync(0xffffffffu, qpart, 1);
+      qpart += __shfl_xor_sync(0xffffffffu, qpart, 2);
+      qpart += __shfl_xor_sync(0xffffffffu, qpart, 4);
+      if (live && (i & 7) == 0) qs[(i >> 3) * MP + n] = -qpart;
+    }
+  } else {
+    // permuted unit layout: one (token, group) per thread, all four lane
+    // classes (no divergence), in place (the thread owns the group's 128 B)
+    for (int job = threadIdx.x; job < gpr * M; job += blockDim.x) {
+      const int n = job / gpr, G = job % gpr;
+      uint8_t* gx = xs + size_t(n) * tok_stride + size_t(G) * 128;
+      const int sh = token_scale(n);
+      const float scale = ldexpf(1.f, sh);
+      if (G == 0) tokscale[n] = ldexpf(1.f, -sh);
+      float xv[64];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4*>(gx + 16 * i);
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) to_f32(wv[q], xv[8 * i + 2 * q], xv[8 * i + 2 * q + 1]);
+      }
+      float qsum = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t out[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const WP w0 = unit_wp(FAM, cc, u, 0), w1 = unit_wp(FAM, cc, u, 1);
+          const __half h0 = __float2half_rn(xv[w0.w] * scale * (1.f / float(1 << w0.p)));
+          const __half h1 = __float2half_rn(xv[w1.w] * scale * (1.f / float(1 << w1.p)));
+          qsum = fmaf(1024.f + float(F::ZP * (1 << w0.p)), __half2float(h0), qsum);
+          qsum = fmaf(1024.f + float(F::ZP * (1 << w1.p)), __half2float(h1), qsum);
+          out[u] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(gx + cc * 32);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+      }
+      qs[G * MP + n] = -qsum;
+    }
+  }
+  // tokens n in [M, MP): -Q = 0 so padded accumulator columns stay zero
+  for (int e = threadIdx.x; e < gpr * (MP - M); e += blockDim.x)
+    qs[(e / (MP - M)) * MP + M + e % (MP - M)] = 0.f;
+  __syncthreads();
+}
 
 template <int FAM, int NT, int S, int XDT, bool P2>
 __global__ void __launch_bounds__(512, 1)
@@ -337,137 +437,9 @@ __global__ void __launch_bounds__(512, 1)
   MTRACE(1, gtime());
 #endif
 
-  // ---- activations: raw rows in by bulk copy, per-token power-of-two scale,
-  //      then converted IN PLACE to f16 (same byte size) ----
   const uint32_t row_bytes = uint32_t(gpr) * 128u;
   const uint32_t tok_stride = row_bytes + 16u;  // +16 B: tokens land in different banks
-  auto to_f32 = [](uint32_t wv, float& lo, float& hi) {
-    if constexpr (XDT == CCQ_DTYPE_BF16) {
-      lo = __uint_as_float(wv << 16);
-      hi = __uint_as_float(wv & 0xFFFF0000u);
-    } else {
-      lo = __half2float(__ushort_as_half(uint16_t(wv & 0xFFFFu)));
-      hi = __half2float(__ushort_as_half(uint16_t(wv >> 16)));
-    }
-  };
-  const int chunks = gpr * 8;  // 16-byte chunks per token
-  {
-    // every thread loads 16-byte chunks of x straight from global memory,
-    // keeps a running max per token and parks the raw bytes in xs
-    float mx[MP];
-#pragma unroll
-    for (int n = 0; n < MP; ++n) mx[n] = 0.f;
-    for (int idx = threadIdx.x; idx < chunks * M; idx += blockDim.x) {
-      const int n = idx / chunks, i = idx - n * chunks;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + int64_t(n) * a.x_ld) + i);
-      *reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16) = v;
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-      float m = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float lo, hi;
-        to_f32(wv[q], lo, hi);
-        m = fmaxf(m, fmaxf(fabsf(lo), fabsf(hi)));
-      }
-#pragma unroll
-      for (int nn = 0; nn < MP; ++nn)
-        if (nn == n) mx[nn] = fmaxf(mx[nn], m);
-    }
-#pragma unroll
-    for (int n = 0; n < MP; ++n) {
-      if (n >= M) break;
-      float m = mx[n];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0 && m > 0.f) atomicMax(&tokmax[n], __float_as_int(fminf(m, 3.0e38f)));
-    }
-  }
-  __syncthreads();
-#ifdef CCQ_GEMV_TRACE
-  MTRACE(2, gtime());
-#endif
-  auto token_scale = [&](int n) {
-    const float mxv = __int_as_float(tokmax[n]);
-    int ex = 0;
-    if (mxv > 0.f) frexpf(mxv, &ex);
-    int sh = mxv > 0.f ? 15 - ex : 0;
-    return sh > 100 ? 100 : (sh < -100 ? -100 : sh);
-  };
-  if constexpr (FAM == kF206) {
-    // natural K order: one 16-byte chunk (8 weights) per thread, in place;
-    // Q of a group = 8 consecutive chunks, combined by shuffles.
-    // Q coefficients: offset (128 for even, 1024 for odd weights) + zero point
-    for (int job0 = threadIdx.x - lane; job0 < chunks * M; job0 += blockDim.x) {
-      const int idx = job0 + lane;
-      const bool live = idx < chunks * M;
-      const int n = live ? idx / chunks : 0, i = live ? idx % chunks : 0;
-      uint4* ptr = reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16);
-      float qpart = 0.f;
-      if (live) {
-        const int sh = token_scale(n);
-        const float scale = ldexpf(1.f, sh);
-        if (i == 0) tokscale[n] = ldexpf(1.f, -sh);
-        const uint4 v = *ptr;
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-        uint32_t o[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float lo, hi;
-          to_f32(wv[q], lo, hi);
-          const __half2 h = __floats2half2_rn(lo * scale, hi * scale);
-          const float2 hf = __half22float2(h);
-          qpart = fmaf(128.f + float(F::ZP), hf.x, qpart);
-          qpart = fmaf(1024.f + float(F::ZP), hf.y, qpart);
-          o[q] = *reinterpret_cast<const uint32_t*>(&h);
-        }
-        *ptr = make_uint4(o[0], o[1], o[2], o[3]);
-      }
-      qpart += __shfl_xor_sync(0xffffffffu, qpart, 1);
-      qpart += __shfl_xor_sync(0xffffffffu, qpart, 2);
-      qpart += __shfl_xor_sync(0xffffffffu, qpart, 4);
-      if (live && (i & 7) == 0) qs[(i >> 3) * MP + n] = -qpart;
-    }
-  } else {
-    // permuted unit layout: one (token, group) per thread, all four lane
-    // classes (no divergence), in place (the thread owns the group's 128 B)
-    for (int job = threadIdx.x; job < gpr * M; job += blockDim.x) {
-      const int n = job / gpr, G = job % gpr;
-      uint8_t* gx = xs + size_t(n) * tok_stride + size_t(G) * 128;
-      const int sh = token_scale(n);
-      const float scale = ldexpf(1.f, sh);
-      if (G == 0) tokscale[n] = ldexpf(1.f, -sh);
-      float xv[64];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint4 v = *reinterpret_cast<const uint4*>(gx + 16 * i);
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) to_f32(wv[q], xv[8 * i + 2 * q], xv[8 * i + 2 * q + 1]);
-      }
-      float qsum = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t out[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const WP w0 = unit_wp(FAM, cc, u, 0), w1 = unit_wp(FAM, cc, u, 1);
-          const __half h0 = __float2half_rn(xv[w0.w] * scale * (1.f / float(1 << w0.p)));
-          const __half h1 = __float2half_rn(xv[w1.w] * scale * (1.f / float(1 << w1.p)));
-          qsum = fmaf(1024.f + float(F::ZP * (1 << w0.p)), __half2float(h0), qsum);
-          qsum = fmaf(1024.f + float(F::ZP * (1 << w1.p)), __half2float(h1), qsum);
-          out[u] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(gx + cc * 32);
-        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
-        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
-      }
-      qs[G * MP + n] = -qsum;
-    }
-  }
-  // tokens n in [M, MP): -Q = 0 so padded accumulator columns stay zero
-  for (int e = threadIdx.x; e < gpr * (MP - M); e += blockDim.x)
-    qs[(e / (MP - M)) * MP + M + e % (MP - M)] = 0.f;
-  __syncthreads();
+  stage_activations<FAM, MP, XDT>(a, xs, qs, tokscale, tokmax, M, gpr, lane);
 #ifdef CCQ_GEMV_TRACE
   MTRACE(3, gtime());
   MTRACE(7, nmine);
@@ -644,6 +616,242 @@ __global__ void __launch_bounds__(512, 1)
 #endif
 }
 
+
+// ---------------------------------------------------------------------------
+// 2.06 "record" variant: the data path of the CUDA-core streaming GEMV (16
+// consecutive (chunk, row) records = ONE contiguous bulk copy per item, as
+// many items in flight as shared memory holds - for the BASELINE shapes the
+// whole CTA's weights are requested at kernel start) with the tensor-pipe
+// decode above.  A dedicated producer warp refills the ring; consumer warps
+// take (item, quarter) units round-robin (8 groups each) and write their
+// partial sums to shared memory; per-(tile, row, token) sums are formed in a
+// fixed order at the end.
+// ---------------------------------------------------------------------------
+template <int NT, int XDT>
+__global__ void __launch_bounds__(416, 1)
+    gemv_rec206(MmaArgs a) {
+  constexpr int FAM = kF206;
+  constexpr int MP = 8 * NT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x >> 5) - 1;  // consumer warps; warp nw is the producer
+  const int g = lane >> 2, c = lane & 3;
+  const int M = a.M, gpr = int(a.gpr), nch = a.nch, S = a.S;
+  const uint32_t rec = a.rec;
+  const uint32_t stg = (16u * rec + 127u) & ~127u;
+
+  const int t_begin = int(int64_t(blockIdx.x) * a.ntiles / gridDim.x);
+  const int t_end = int(int64_t(blockIdx.x + 1) * a.ntiles / gridDim.x);
+  const int ntl = t_end - t_begin;
+  const int items = ntl * nch, units = items * 4;
+
+  uint8_t* ring = smem;
+  uint8_t* xs = ring + size_t(S) * stg;
+  float* qs = reinterpret_cast<float*>(xs + a.xs_bytes);
+  float* part = qs + a.gpr * MP;                                     // [units][16][MP]
+  float* tokscale = part + size_t(units) * kRowsT * MP;
+  int* tokmax = reinterpret_cast<int*>(tokscale + MP);
+  uint8_t* zblk = reinterpret_cast<uint8_t*>(tokmax + MP);           // 128 B zeros
+  uint64_t* full = reinterpret_cast<uint64_t*>(zblk + 128);
+  uint64_t* empty = full + S;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+  }
+  if (threadIdx.x < MP) tokmax[threadIdx.x] = 0;
+  if (threadIdx.x < 32) reinterpret_cast<int*>(zblk)[threadIdx.x] = 0;
+  fence_mbar_init();
+  __syncthreads();
+
+  const bool producer = warp == nw;
+  auto produce = [&](int i) {
+    const int s = i % S;
+    const int tile = t_begin + i / nch, chunk = i % nch;
+    if (i >= S) mbar_wait(&empty[s], uint32_t(((i / S) - 1) & 1));
+    mbar_arrive_expect_tx(&full[s], 16u * rec);
+    bulk_g2s(ring + size_t(s) * stg, a.codes + (uint64_t(chunk) * a.rows_pad + uint64_t(tile) * kRowsT) * rec,
+             16u * rec, &full[s]);
+  };
+  // weights do not depend on the previous kernel: first S items go out now
+  if (producer && lane == 0)
+    for (int i = 0; i < S && i < items; ++i) produce(i);
+  griddep_launch_dependents();
+  griddep_wait();
+
+  stage_activations<FAM, MP, XDT>(a, xs, qs, tokscale, tokmax, M, gpr, lane);
+
+  if (producer) {
+    if (lane == 0)
+      for (int i = S; i < items; ++i) produce(i);
+  } else {
+    const uint32_t row_bytes = uint32_t(gpr) * 128u, tok_stride = row_bytes + 16u;
+    const uint8_t* xb[NT];
+    uint32_t gstride[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int nb = nt * 8 + g;
+      const bool live = nb < M;
+      xb[nt] = live ? xs + size_t(nb) * tok_stride + c * 32 : zblk + c * 32;
+      gstride[nt] = live ? 128u : 0u;
+    }
+    const float* qlane = qs + 2 * c;
+#pragma unroll 1
+    for (int u = warp; u < units; u += nw) {
+      const int item = u >> 2, q = u & 3;
+      const int s = item % S;
+      mbar_wait(&full[s], uint32_t((item / S) & 1));
+      const uint8_t* st = ring + size_t(s) * stg;
+      const int chunk = item % nch;
+      RowCtx rc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint8_t* rr = st + (g + 8 * h) * rec;
+        const uint4 pv = *reinterpret_cast<const uint4*>(rr + a.rec - 16);
+        rc[h].C = (uint64_t(pv.x) | (uint64_t(pv.y) << 32)) >> 8;
+        rc[h].M = pv.z;
+        uint32_t step = pv.w >> 16;
+        step = step > 1u ? step >> 4 : 1u;
+        const uint32_t pos = step == 1u ? 0u : step == 16u ? 1u : step == 256u ? 2u : 3u;
+        const uint32_t base = (0x4444u & ~(0xFu << (4u * pos))) & 0xFFFFu;
+        rc[h].sel[0] = base;
+        rc[h].sel[1] = base + step;
+        rc[h].sel[2] = base + 2 * step;
+        rc[h].sel[3] = base + 3 * step;
+        rc[h].nib = *reinterpret_cast<const uint32_t*>(rr + a.rec - 32 + 4 * q);
+      }
+      float yacc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) yacc[nt][i] = 0.f;
+      const int G0 = chunk * kChunk + 8 * q;
+      auto group = [&](int j) {
+        const int G = G0 + j;
+        uint32_t ua[8], ub[8];
+        const uint8_t* p = st + g * rec + (8 * q + j) * 16 + 4 * c;
+        const uint32_t sca = decode_units<FAM, true>(p, g, j, c, rc[0], ua);
+        const uint32_t scb = decode_units<FAM, true>(p + 8 * rec, g + 8, j, c, rc[1], ub);
+        const float fa = float(sca), fb = float(scb);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const float2 q2 = *reinterpret_cast<const float2*>(qlane + G * MP + nt * 8);
+          float d[4] = {q2.x, q2.y, q2.x, q2.y};
+          const uint4* src = reinterpret_cast<const uint4*>(xb[nt] + uint32_t(G) * gstride[nt]);
+          const uint4 b01 = src[0], b23 = src[1];
+          const uint32_t bb[8] = {b01.x, b01.y, b01.z, b01.w, b23.x, b23.y, b23.z, b23.w};
+          float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t af[4] = {ua[2 * t], ub[2 * t], ua[2 * t + 1], ub[2 * t + 1]};
+            if (t & 1) mma16816(e, af, bb[2 * t], bb[2 * t + 1]);
+            else mma16816(d, af, bb[2 * t], bb[2 * t + 1]);
+          }
+          yacc[nt][0] = fmaf(fa, d[0] + e[0], yacc[nt][0]);
+          yacc[nt][1] = fmaf(fa, d[1] + e[1], yacc[nt][1]);
+          yacc[nt][2] = fmaf(fb, d[2] + e[2], yacc[nt][2]);
+          yacc[nt][3] = fmaf(fb, d[3] + e[3], yacc[nt][3]);
+        }
+      };
+      if (gpr - G0 >= 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) group(j);
+      } else {
+#pragma unroll 1
+        for (int j = 0; j < gpr - G0; ++j) group(j);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this quarter no longer reads the stage
+      float* pp = part + size_t(u) * kRowsT * MP;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n0 = nt * 8 + 2 * c;
+        *reinterpret_cast<float2*>(pp + g * MP + n0) = make_float2(yacc[nt][0], yacc[nt][1]);
+        *reinterpret_cast<float2*>(pp + (g + 8) * MP + n0) = make_float2(yacc[nt][2], yacc[nt][3]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ntl * kRowsT * M; e += blockDim.x) {
+    const int tl = e / (kRowsT * M), rem = e % (kRowsT * M);
+    const int r = rem / M, n = rem % M;
+    const int64_t row = int64_t(t_begin + tl) * kRowsT + r;
+    if (row >= a.rows) continue;
+    float v = 0.f;
+    for (int ui = tl * nch * 4; ui < (tl + 1) * nch * 4; ++ui) v += part[(size_t(ui) * kRowsT + r) * MP + n];
+    v *= a.super[row] * tokscale[n];
+    if (a.y_dtype == CCQ_DTYPE_F32)
+      static_cast<float*>(a.y)[int64_t(n) * a.y_ld + row] = v;
+    else
+      static_cast<__nv_bfloat16*>(a.y)[int64_t(n) * a.y_ld + row] = __float2bfloat16_rn(v);
+  }
+}
+
+// Shared-memory plan of the record variant; S = 0 when it does not apply.
+struct RecCfg {
+  int S;
+  size_t smem;
+};
+inline RecCfg rec_cfg(const ccq_dev_model* m, int M, int grid, int max_smem) {
+  const int MP = M > 8 ? 16 : 8;
+  const int ntiles = int((m->rows + kRowsT - 1) / kRowsT);
+  const int tiles_cta = (ntiles + grid - 1) / grid;
+  const int items = tiles_cta * m->nch;
+  const size_t stg = (size_t(16) * m->rec + 127) & ~size_t(127);
+  const size_t fixed = size_t(m->gpr * 128 + 16) * M + size_t(m->gpr) * MP * 4 +
+                       size_t(items) * 4 * kRowsT * MP * 4 + MP * 8 + 128 + 256;
+  if (fixed + 2 * stg + size_t(items) * 16 > size_t(max_smem)) return RecCfg{0, 0};
+  const int S = int(std::min<size_t>(size_t(items), (size_t(max_smem) - fixed) / (stg + 16)));
+  return RecCfg{S, fixed + size_t(S) * (stg + 16)};
+}
+
+template <int NT, int XDT>
+int launch_rec(const ccq_dev_model* m, const void* x, int M, void* y, int x_dtype, int y_dtype, int grid,
+               const RecCfg& cfg, cudaStream_t s) {
+  MmaArgs a{};
+  a.super = m->super;
+  a.plan = m->plan;
+  a.x = x;
+  a.y = y;
+  a.x_dtype = x_dtype;
+  a.y_dtype = y_dtype;
+  a.M = M;
+  a.rows = m->rows;
+  a.rows_pad = m->rows_pad;
+  a.gpr = m->gpr;
+  a.ntiles = int((m->rows + kRowsT - 1) / kRowsT);
+  a.x_ld = m->cols;
+  a.y_ld = m->rows;
+  a.xs_bytes = uint32_t((m->gpr * 128 + 16) * M);
+  a.codes = m->codes;
+  a.rec = m->rec;
+  a.nch = m->nch;
+  a.S = cfg.S;
+  auto kern = gemv_rec206<NT, XDT>;
+  static size_t configured[3][3] = {};
+  size_t& conf = configured[NT][XDT];
+  if (conf < cfg.smem) {
+    CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)));
+    conf = cfg.smem;
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(unsigned(grid));
+  lc.blockDim = dim3(13u * 32u);
+  lc.dynamicSmemBytes = cfg.smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
+  count_launch();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemv_rec206 launch");
+}
+
 struct Cfg {
   int warps, slots;
   size_t smem;
@@ -766,6 +974,24 @@ int launch_fam_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
 
 }  // namespace
 
+// True when all M tokens fit one launch with >= 8 warps per CTA (no weight re-streaming).
+bool gemv_mma_fits(const ccq_dev_model* m, int64_t M) {
+  if (M < 1 || M > 8 || !gemv_mma_supported(m, M)) return false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int ntiles = int((m->rows + 15) / 16);
+  const int grid = std::min(num_sms(dev), ntiles);
+  Cfg cfg{};
+  switch (m->family) {
+    case kF275: cfg = plan_cfg<kF275, 1, 4>(m, int(M), grid, max_smem); break;
+    case kF25: cfg = plan_cfg<kF25, 1, 4>(m, int(M), grid, max_smem); break;
+    default: cfg = plan_cfg<kF206, 1, 4>(m, int(M), grid, max_smem); break;
+  }
+  return cfg.warps >= 8;
+}
+
 int mma_min_tokens() {
   const char* e = std::getenv("CCQ_FORCE_MMA");
   return (e && e[0] == '1') ? 1 : kMmaMinTokens;
@@ -786,9 +1012,25 @@ int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   switch (m->family) {
     case kF275: return launch_fam_mma<kF275, false>(m, x, x_dtype, M, y, y_dtype, s);
     case kF25: return launch_fam_mma<kF25, false>(m, x, x_dtype, M, y, y_dtype, s);
-    default:
+    default: {
+      if (m->plan_pos_min >= 1 && M <= 16 && m->rec == uint32_t(m->cgb + 32) && !std::getenv("CCQ_NO_REC")) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int max_smem = 0;
+        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int grid = std::min<int>(num_sms(dev), int((m->rows + kRowsT - 1) / kRowsT));
+        const RecCfg rc = rec_cfg(m, int(M), grid, max_smem);
+        if (rc.S > 0) {
+          if (M > 8)
+            return x_dtype == CCQ_DTYPE_BF16 ? launch_rec<2, CCQ_DTYPE_BF16>(m, x, int(M), y, x_dtype, y_dtype, grid, rc, s)
+                                             : launch_rec<2, CCQ_DTYPE_F16>(m, x, int(M), y, x_dtype, y_dtype, grid, rc, s);
+          return x_dtype == CCQ_DTYPE_BF16 ? launch_rec<1, CCQ_DTYPE_BF16>(m, x, int(M), y, x_dtype, y_dtype, grid, rc, s)
+                                           : launch_rec<1, CCQ_DTYPE_F16>(m, x, int(M), y, x_dtype, y_dtype, grid, rc, s);
+        }
+      }
       return m->plan_pos_min >= 1 ? launch_fam_mma<kF206, true>(m, x, x_dtype, M, y, y_dtype, s)
                                   : launch_fam_mma<kF206, false>(m, x, x_dtype, M, y, y_dtype, s);
+    }
   }
 }
 

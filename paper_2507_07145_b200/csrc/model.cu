@@ -370,8 +370,10 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   // to kMmaMaxTokens tokens; beyond that the tcgen05 GEMM (2.06) takes over.
   const bool mma = x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
                    gemv_mma_supported(m, M);
-  // (M = 1 on the CUDA-core streaming kernel: measured faster, profiles/r01_*)
-  if (mma && M >= mma_min_tokens() && (M <= kMmaMaxTokens || !gemm_supported(m, M)))
+  // Measured (profiles/r01_sweep_*): M = 1 on the CUDA-core streaming GEMV;
+  // 2 <= M <= 8 on the tensor-pipe GEMV when all tokens fit one launch; the
+  // tcgen05 GEMM above that (or when the activations would not fit).
+  if (mma && M >= mma_min_tokens() && (gemv_mma_fits(m, M) || !gemm_supported(m, M)))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
   if (!gemv_fast_supported(m, M) && gemm_supported(m, M))
     return launch_gemm(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));

@@ -286,12 +286,15 @@ def test_baseline_shape_full_size(oracle, ccq, cuda, fam):
 
 # ------------------------------------------------------------ gemm (c) tcgen05 --
 
+@pytest.mark.parametrize("fam", [0, 1, 2])
 @pytest.mark.parametrize("shape", [(128, 512), (200, 4096), (384, 2048 + 64), (130, 14336), (64, 192)])
 @pytest.mark.parametrize("M", [9, 32, 64, 100, 128, 256, 300])
-def test_gemm_tcgen05_206_bf16(oracle, ccq, cuda, shape, M):
+def test_gemm_tcgen05_bf16(oracle, ccq, cuda, fam, shape, M):
+    """All three families on tcgen05: exact f16 weight operands (2.5 as two
+    exact parts with two TMEM accumulators), f32 accumulation."""
     torch = cuda
     rows, cols = shape
-    s = oracle.random_packed(rows, cols, 2, 64, seed=rows + cols + M)
+    s = oracle.random_packed(rows, cols, fam, 64, seed=rows + cols + M + fam)
     d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
     x = oracle.random_matrix(M, cols, "gaussian", 17 + M)
     xb = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
@@ -301,8 +304,9 @@ def test_gemm_tcgen05_206_bf16(oracle, ccq, cuda, shape, M):
     assert rel_err(y.cpu().numpy(), want) < REL_TOL
 
 
-def test_gemm_tcgen05_f32_input_within_contract(oracle, ccq, cuda):
-    s = oracle.random_packed(256, 1024, 2, 64, seed=3)
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_gemm_tcgen05_f32_input_within_contract(oracle, ccq, cuda, fam):
+    s = oracle.random_packed(256, 1024, fam, 64, seed=3)
     d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
     x = oracle.random_matrix(64, 1024, "gaussian", 5)
     y = ccq.gemv_batch(d, x)  # M = 64 dispatches to the tcgen05 GEMM
@@ -310,21 +314,23 @@ def test_gemm_tcgen05_f32_input_within_contract(oracle, ccq, cuda):
     assert rel_err(y, oracle.gemv_batch(s, x, threads=8)) < REL_TOL
 
 
+@pytest.mark.parametrize("fam", [0, 1, 2])
 @pytest.mark.parametrize("M", [1, 3, 31, 33, 200])
 @pytest.mark.parametrize("scale", [1.0, 1e-6, 3e5])
-def test_gemm_f32_input_scaling(oracle, ccq, cuda, M, scale):
+def test_gemm_f32_input_scaling(oracle, ccq, cuda, fam, M, scale):
     """Per-token power-of-two scaling: tiny and huge activations stay exact."""
     torch = cuda
-    s = oracle.random_packed(160, 1024, 2, 64, seed=M)
+    s = oracle.random_packed(160, 1024, fam, 64, seed=M + fam)
     d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
     x = (oracle.random_matrix(M, 1024, "gaussian", 40 + M) * np.float32(scale)).astype(np.float32)
     y = ccq.matmul(d, torch.from_numpy(x).cuda(), kernel="gemm")
     assert rel_err(y.cpu().numpy(), oracle.gemv_batch(s, x, threads=8)) < REL_TOL
 
 
-def test_gemm_bf16_output(oracle, ccq, cuda):
+@pytest.mark.parametrize("fam", [0, 1, 2])
+def test_gemm_bf16_output(oracle, ccq, cuda, fam):
     torch = cuda
-    s = oracle.random_packed(256, 1024, 2, 64, seed=4)
+    s = oracle.random_packed(256, 1024, fam, 64, seed=4)
     d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
     x = oracle.random_matrix(48, 1024, "gaussian", 6)
     xb = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
