@@ -274,11 +274,15 @@ def main():
         e2e_ms = float(t.item())
     e2e_val = bytes_step * world / (e2e_ms * 1e-3) / 1e9
 
-    sweep = prefill = None
+    sweep = prefill = moe = paper = None
     tflops_peak = float(peaks.get("bf16_tflops", 1590.0))
     if args.sweep and rank == 0:
         sweep = run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak)
-        prefill = run_prefill(P, torch, dev, stream, tflops_peak)
+        paper = run_paper_shapes(P, torch, dev, stream)
+        with ClockSampler(local) as pclk:
+            prefill = run_prefill(P, torch, dev, stream, tflops_peak)
+        prefill = {"runs": prefill, "clocks": pclk.summary()}
+        moe = run_moe(P, torch, dev, stream, hbm_peak, tflops_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -326,6 +330,10 @@ def main():
             out["sweep"] = sweep
         if prefill is not None:
             out["prefill"] = prefill
+        if moe is not None:
+            out["moe"] = moe
+        if paper is not None:
+            out["paper_shapes"] = paper
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
@@ -379,6 +387,87 @@ def run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak):
                             "TFLOPs": round(tf, 2), "tensor_frac": round(tf / tflops_peak, 4)})
             del ms_
     return res
+
+
+def _graph_time_us(torch, stream, body, reps=10):
+    with torch.cuda.stream(stream):
+        body()
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        body()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        s1.record(stream)
+    torch.cuda.synchronize()
+    return s0.elapsed_time(s1) * 1e3 / reps
+
+
+def run_moe(P, torch, dev, stream, hbm_peak, tflops_peak):
+    """BASELINE configs[2] / [3] on one GPU: ERNIE-4.5 64 experts 8192->3584 and
+    DeepSeek-V3 256 experts 7168->2048, CCQ 2.06, top-8 uniform routing
+    (8 distinct experts per token), decode batch B tokens.  Packed bytes count
+    only experts with >= 1 routed token."""
+    import numpy as np
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    out = []
+    for name, E, din, dout in (("ERNIE-4.5-300B-A47B", 64, 8192, 3584), ("DeepSeek-V3", 256, 7168, 2048)):
+        models = [_synthetic(dout, din, 2, 64, 1000 + e) for e in range(E)]
+        pb_e = P.model_payload_bytes(models[0])
+        ex = P.Experts.upload(models, device=dev.index)
+        del models
+        rng = np.random.default_rng(7)
+        for B in (1, 16, 64, 256):
+            counts = np.zeros(E, np.int64)
+            for _ in range(B):
+                counts[rng.choice(E, 8, replace=False)] += 1
+            offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+            T = int(offs[-1])
+            offs_dev = torch.from_numpy(offs).to(dev)
+            x = torch.randn(T, din, device=dev).to(torch.bfloat16)
+            y = torch.empty(T, dout, device=dev)
+            us = _graph_time_us(torch, stream, lambda: P.experts_matmul(ex, offs, x, out=y, stream=stream,
+                                                                          offsets_dev=offs_dev))
+            routed = int((counts > 0).sum())
+            gbs = routed * pb_e / us / 1e3
+            tf = 2 * T * din * dout / us / 1e6
+            out.append({"model": name, "experts": E, "d_in": din, "d_out": dout, "batch": B, "routed_pairs": T,
+                        "experts_hit": routed, "us": round(us, 2), "tokens_per_s": round(B / us * 1e6, 1),
+                        "packed_GBps_routed": round(gbs, 1), "hbm_frac": round(gbs / hbm_peak, 4),
+                        "TFLOPs": round(tf, 2), "tensor_frac": round(tf / tflops_peak, 4)})
+        del ex
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_paper_shapes(P, torch, dev, stream):
+    """The four GEMV shapes of the paper's H20 table, 2.06,
+    M = 1 and 4, for context (different GPU; not a vs_baseline ratio)."""
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    h20 = {(4096, 4096): (34.0, 35.0), (4096, 1024): (17.0, 17.0), (8192, 8192): (90.0, 104.0),
+           (8192, 1024): (22.0, 24.0)}
+    out = []
+    for (din, dout), (t1, t4) in h20.items():
+        copies = max(2, int(160e6 // (din * dout * 0.26)) + 1)
+        ms_ = [P.DeviceModel.upload(_synthetic(dout, din, 2, 64, 3 + c), device=dev.index) for c in range(copies)]
+        for M, th in ((1, t1), (4, t4)):
+            x = torch.randn(M, din, device=dev).to(torch.bfloat16)
+            y = torch.empty(M, dout, device=dev)
+
+            def body():
+                for mm in ms_:
+                    P.matmul(mm, x, out=y, stream=stream)
+            us = _graph_time_us(torch, stream, body) / copies
+            out.append({"d_in": din, "d_out": dout, "M": M, "us": round(us, 3), "paper_h20_us": th,
+                        "speedup_vs_h20_table": round(th / us, 2)})
+        del ms_
+    return out
 
 
 def run_prefill(P, torch, dev, stream, tflops_peak):

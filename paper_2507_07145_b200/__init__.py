@@ -399,15 +399,19 @@ class Experts(DeviceModel):
         return ex
 
 
-def experts_matmul(experts: "Experts", offsets, x, out=None, out_dtype=None, stream=None):
-    """y[T, rows_per_expert] for expert-major tokens x[T, cols]."""
+def experts_matmul(experts: "Experts", offsets, x, out=None, out_dtype=None, stream=None,
+                   offsets_dev=None):
+    """y[T, rows_per_expert] for expert-major tokens x[T, cols].
+
+    `offsets` (E+1 host ints) sizes the launch; `offsets_dev` (the same values
+    as a device int32 tensor) may be passed to skip the per-call upload."""
     import torch
     offs = np.ascontiguousarray(np.asarray(offsets, np.int32))
     if offs.size != experts.num_experts + 1:
         raise ShapeError("offsets must have num_experts+1 entries")
     if not x.is_contiguous() or x.dim() != 2 or x.shape[1] != experts.cols or x.shape[0] < offs[-1]:
         raise ShapeError("activations must be contiguous [offsets[-1], cols]")
-    offs_dev = torch.from_numpy(offs).to(x.device)
+    offs_dev = offsets_dev if offsets_dev is not None else torch.from_numpy(offs).to(x.device)
     if out is None:
         out = torch.empty(int(offs[-1]), experts.rows_per_expert, dtype=out_dtype or torch.float32,
                           device=x.device)
