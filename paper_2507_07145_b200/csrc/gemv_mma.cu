@@ -43,6 +43,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "ccq_internal.hpp"
 #include "ptx.cuh"
@@ -215,6 +216,11 @@ struct MmaArgs {
   uint32_t rec;
   int nch;
   int S;
+  // grouped experts (gemv_rec206<.., true>): E stacked experts of rows_e rows,
+  // tokens expert-major with offsets[E+1] (device); only experts with tokens run
+  const int32_t* offsets;
+  int E;
+  int64_t rows_e;
 };
 
 // Activations -> shared memory in the f16 operand layout of the family (see
@@ -222,7 +228,7 @@ struct MmaArgs {
 // Called by every thread of the CTA (contains __syncthreads).
 template <int FAM, int MP, int XDT>
 __device__ __forceinline__ void stage_activations(const MmaArgs& a, uint8_t* xs, float* qs, float* tokscale,
-                                                  int* tokmax, int M, int gpr, int lane) {
+                                                  int* tokmax, int M, int gpr, int lane, int tok0 = 0) {
   using F = MF<FAM>;
   // ---- activations: raw rows in by bulk copy, per-token power-of-two scale,
   //      then converted IN PLACE to f16 (same byte size) ----
@@ -246,7 +252,7 @@ __device__ __forceinline__ void stage_activations(const MmaArgs& a, uint8_t* xs,
     for (int n = 0; n < MP; ++n) mx[n] = 0.f;
     for (int idx = threadIdx.x; idx < chunks * M; idx += blockDim.x) {
       const int n = idx / chunks, i = idx - n * chunks;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + int64_t(n) * a.x_ld) + i);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + int64_t(tok0 + n) * a.x_ld) + i);
       *reinterpret_cast<uint4*>(xs + size_t(n) * tok_stride + size_t(i) * 16) = v;
       const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
       float m = 0.f;
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(512, 1)
 // partial sums to shared memory; per-(tile, row, token) sums are formed in a
 // fixed order at the end.
 // ---------------------------------------------------------------------------
-template <int NT, int XDT>
+template <int NT, int XDT, bool GROUPED>
 __global__ void __launch_bounds__(416, 1)
     gemv_rec206(MmaArgs a) {
   constexpr int FAM = kF206;
@@ -640,10 +646,59 @@ __global__ void __launch_bounds__(416, 1)
   const uint32_t rec = a.rec;
   const uint32_t stg = (16u * rec + 127u) & ~127u;
 
-  const int t_begin = int(int64_t(blockIdx.x) * a.ntiles / gridDim.x);
-  const int t_end = int(int64_t(blockIdx.x + 1) * a.ntiles / gridDim.x);
+  // grouped: compact the experts that have tokens (hit[]), their tiles are the work
+  __shared__ int hit[256];
+  __shared__ int nhit_s, wsum[16];
+  int ntiles = a.ntiles;
+  const int tpe = GROUPED ? int(a.rows_e / kRowsT) : 1;
+  if constexpr (GROUPED) {
+    const int e = threadIdx.x;
+    const bool has = e < a.E && a.offsets[e + 1] > a.offsets[e];
+    const unsigned bal = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) { const int t = wsum[w]; wsum[w] = acc; acc += t; }
+      nhit_s = acc;
+    }
+    __syncthreads();
+    if (has) hit[wsum[warp] + __popc(bal & ((1u << lane) - 1u))] = e;
+    __syncthreads();
+    ntiles = nhit_s * tpe;
+  }
+  // (tile index within this launch) -> stack row of its first row, expert, token range
+  auto tile_info = [&](int t, int64_t& row0, int& off, int& cnt) {
+    if constexpr (GROUPED) {
+      const int e = hit[t / tpe];
+      row0 = int64_t(e) * a.rows_e + int64_t(t % tpe) * kRowsT;
+      off = a.offsets[e];
+      cnt = a.offsets[e + 1] - off;
+    } else {
+      row0 = int64_t(t) * kRowsT;
+      off = 0;
+      cnt = a.M;
+    }
+  };
+  const int t_begin = int(int64_t(blockIdx.x) * ntiles / gridDim.x);
+  const int t_end = int(int64_t(blockIdx.x + 1) * ntiles / gridDim.x);
   const int ntl = t_end - t_begin;
   const int items = ntl * nch, units = items * 4;
+  // grouped: this CTA stages only the tokens of the experts its tiles belong to
+  // (expert-major layout: one contiguous window [tok0, tok0 + Mc))
+  int tok0 = 0, Mc = M;
+  if constexpr (GROUPED) {
+    if (ntl > 0) {
+      int64_t r0;
+      int o0, c0, o1, c1;
+      tile_info(t_begin, r0, o0, c0);
+      tile_info(t_end - 1, r0, o1, c1);
+      tok0 = o0;
+      Mc = o1 + c1 - o0;
+    } else {
+      Mc = 0;
+    }
+  }
 
   uint8_t* ring = smem;
   uint8_t* xs = ring + size_t(S) * stg;
@@ -669,10 +724,13 @@ __global__ void __launch_bounds__(416, 1)
   const bool producer = warp == nw;
   auto produce = [&](int i) {
     const int s = i % S;
-    const int tile = t_begin + i / nch, chunk = i % nch;
+    const int chunk = i % nch;
+    int64_t row0;
+    int off, cnt;
+    tile_info(t_begin + i / nch, row0, off, cnt);
     if (i >= S) mbar_wait(&empty[s], uint32_t(((i / S) - 1) & 1));
     mbar_arrive_expect_tx(&full[s], 16u * rec);
-    bulk_g2s(ring + size_t(s) * stg, a.codes + (uint64_t(chunk) * a.rows_pad + uint64_t(tile) * kRowsT) * rec,
+    bulk_g2s(ring + size_t(s) * stg, a.codes + (uint64_t(chunk) * a.rows_pad + uint64_t(row0)) * rec,
              16u * rec, &full[s]);
   };
   // weights do not depend on the previous kernel: first S items go out now
@@ -681,26 +739,30 @@ __global__ void __launch_bounds__(416, 1)
   griddep_launch_dependents();
   griddep_wait();
 
-  stage_activations<FAM, MP, XDT>(a, xs, qs, tokscale, tokmax, M, gpr, lane);
+  stage_activations<FAM, MP, XDT>(a, xs, qs, tokscale, tokmax, Mc, gpr, lane, tok0);
 
   if (producer) {
     if (lane == 0)
       for (int i = S; i < items; ++i) produce(i);
   } else {
     const uint32_t row_bytes = uint32_t(gpr) * 128u, tok_stride = row_bytes + 16u;
-    const uint8_t* xb[NT];
-    uint32_t gstride[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int nb = nt * 8 + g;
-      const bool live = nb < M;
-      xb[nt] = live ? xs + size_t(nb) * tok_stride + c * 32 : zblk + c * 32;
-      gstride[nt] = live ? 128u : 0u;
-    }
-    const float* qlane = qs + 2 * c;
 #pragma unroll 1
     for (int u = warp; u < units; u += nw) {
       const int item = u >> 2, q = u & 3;
+      int64_t row0;
+      int toff, tcnt;
+      tile_info(t_begin + item / nch, row0, toff, tcnt);
+      toff -= tok0;  // row of the staged window
+      const uint8_t* xb[NT];
+      uint32_t gstride[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int nb = nt * 8 + g;
+        const bool live = nb < tcnt;
+        xb[nt] = live ? xs + size_t(toff + nb) * tok_stride + c * 32 : zblk + c * 32;
+        gstride[nt] = live ? 128u : 0u;
+      }
+      const float* qlane = qs + toff + 2 * c;
       const int s = item % S;
       mbar_wait(&full[s], uint32_t((item / S) & 1));
       const uint8_t* st = ring + size_t(s) * stg;
@@ -737,8 +799,9 @@ __global__ void __launch_bounds__(416, 1)
         const float fa = float(sca), fb = float(scb);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const float2 q2 = *reinterpret_cast<const float2*>(qlane + G * MP + nt * 8);
-          float d[4] = {q2.x, q2.y, q2.x, q2.y};
+          // token offset may be odd (grouped experts): two scalar loads, not a float2
+          const float q0 = qlane[G * MP + nt * 8], q1 = qlane[G * MP + nt * 8 + 1];
+          float d[4] = {q0, q1, q0, q1};
           const uint4* src = reinterpret_cast<const uint4*>(xb[nt] + uint32_t(G) * gstride[nt]);
           const uint4 b01 = src[0], b23 = src[1];
           const uint32_t bb[8] = {b01.x, b01.y, b01.z, b01.w, b23.x, b23.y, b23.z, b23.w};
@@ -774,18 +837,24 @@ __global__ void __launch_bounds__(416, 1)
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < ntl * kRowsT * M; e += blockDim.x) {
-    const int tl = e / (kRowsT * M), rem = e % (kRowsT * M);
-    const int r = rem / M, n = rem % M;
-    const int64_t row = int64_t(t_begin + tl) * kRowsT + r;
-    if (row >= a.rows) continue;
+  for (int e = threadIdx.x; e < ntl * kRowsT * MP; e += blockDim.x) {
+    const int tl = e / (kRowsT * MP), rem = e % (kRowsT * MP);
+    const int r = rem / MP, n = rem % MP;
+    int64_t row0;
+    int toff, tcnt;
+    tile_info(t_begin + tl, row0, toff, tcnt);
+    const int64_t row = row0 + r;
+    if (n >= tcnt || row >= a.rows) continue;
     float v = 0.f;
     for (int ui = tl * nch * 4; ui < (tl + 1) * nch * 4; ++ui) v += part[(size_t(ui) * kRowsT + r) * MP + n];
-    v *= a.super[row] * tokscale[n];
+    v *= a.super[row] * tokscale[toff - tok0 + n];
+    // y: plain [M][rows]; grouped: expert-major tokens x rows_e
+    const int64_t yi = GROUPED ? int64_t(toff + n) * a.rows_e + (row - (row0 - row0 % a.rows_e))
+                               : int64_t(n) * a.y_ld + row;
     if (a.y_dtype == CCQ_DTYPE_F32)
-      static_cast<float*>(a.y)[int64_t(n) * a.y_ld + row] = v;
+      static_cast<float*>(a.y)[yi] = v;
     else
-      static_cast<__nv_bfloat16*>(a.y)[int64_t(n) * a.y_ld + row] = __float2bfloat16_rn(v);
+      static_cast<__nv_bfloat16*>(a.y)[yi] = __float2bfloat16_rn(v);
   }
 }
 
@@ -794,9 +863,10 @@ struct RecCfg {
   int S;
   size_t smem;
 };
-inline RecCfg rec_cfg(const ccq_dev_model* m, int M, int grid, int max_smem) {
+inline RecCfg rec_cfg(const ccq_dev_model* m, int M, int grid, int max_smem, int ntiles_override = -1) {
   const int MP = M > 8 ? 16 : 8;
-  const int ntiles = int((m->rows + kRowsT - 1) / kRowsT);
+  max_smem -= 2048;  // static shared memory of the kernel (expert list)
+  const int ntiles = ntiles_override >= 0 ? ntiles_override : int((m->rows + kRowsT - 1) / kRowsT);
   const int tiles_cta = (ntiles + grid - 1) / grid;
   const int items = tiles_cta * m->nch;
   const size_t stg = (size_t(16) * m->rec + 127) & ~size_t(127);
@@ -807,9 +877,10 @@ inline RecCfg rec_cfg(const ccq_dev_model* m, int M, int grid, int max_smem) {
   return RecCfg{S, fixed + size_t(S) * (stg + 16)};
 }
 
-template <int NT, int XDT>
+template <int NT, int XDT, bool GROUPED = false>
 int launch_rec(const ccq_dev_model* m, const void* x, int M, void* y, int x_dtype, int y_dtype, int grid,
-               const RecCfg& cfg, cudaStream_t s) {
+               const RecCfg& cfg, cudaStream_t s, const int32_t* offsets = nullptr, int E = 0,
+               int64_t rows_e = 0) {
   MmaArgs a{};
   a.super = m->super;
   a.plan = m->plan;
@@ -829,9 +900,12 @@ int launch_rec(const ccq_dev_model* m, const void* x, int M, void* y, int x_dtyp
   a.rec = m->rec;
   a.nch = m->nch;
   a.S = cfg.S;
-  auto kern = gemv_rec206<NT, XDT>;
-  static size_t configured[3][3] = {};
-  size_t& conf = configured[NT][XDT];
+  a.offsets = offsets;
+  a.E = E;
+  a.rows_e = rows_e;
+  auto kern = gemv_rec206<NT, XDT, GROUPED>;
+  static size_t configured[3][3][2] = {};
+  size_t& conf = configured[NT][XDT][GROUPED ? 1 : 0];
   if (conf < cfg.smem) {
     CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)));
     conf = cfg.smem;
@@ -990,6 +1064,50 @@ bool gemv_mma_fits(const ccq_dev_model* m, int64_t M) {
     default: cfg = plan_cfg<kF206, 1, 4>(m, int(M), grid, max_smem); break;
   }
   return cfg.warps >= 8;
+}
+
+// Kernel (d) for decode batches: all routed (expert, token) rows in ONE
+// tensor-pipe GEMV launch over the tiles of the experts that have tokens.
+// Returns 1 when not applicable (caller falls back to the grouped GEMM).
+int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev,
+                        const int32_t* offsets_host, int64_t T, const void* x, int x_dtype, void* y,
+                        int y_dtype, cudaStream_t s) {
+  if (st->family != kF206 || st->plan_pos_min < 1 || T < 1 || E > 256 || rows_e % kRowsT != 0 ||
+      st->geo.group_size != 64 || st->cols % 64 != 0 || st->rec != uint32_t(st->cgb + 32) ||
+      x_dtype == CCQ_DTYPE_F32 || (reinterpret_cast<uintptr_t>(x) & 15u) || !offsets_dev ||
+      std::getenv("CCQ_NO_GROUPED_GEMV"))
+    return 1;
+  int nhit = 0;
+  for (int e = 0; e < E; ++e) nhit += offsets_host[e + 1] > offsets_host[e] ? 1 : 0;
+  if (nhit == 0) return CCQ_OK;
+  const int tpe = int(rows_e / kRowsT);
+  const int ntiles = nhit * tpe;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int grid = std::min(num_sms(dev), ntiles);
+  // the largest token window any CTA stages (same partition as the kernel)
+  std::vector<int> hits;
+  for (int e = 0; e < E; ++e)
+    if (offsets_host[e + 1] > offsets_host[e]) hits.push_back(e);
+  int wmax = 1;
+  for (int b = 0; b < grid; ++b) {
+    const int tb = int(int64_t(b) * ntiles / grid), te = int(int64_t(b + 1) * ntiles / grid);
+    if (te <= tb) continue;
+    const int e0 = hits[tb / tpe], e1 = hits[(te - 1) / tpe];
+    wmax = std::max(wmax, offsets_host[e1 + 1] - offsets_host[e0]);
+  }
+  if (wmax > 16) return 1;  // some expert (or CTA window) has too many tokens: grouped GEMM
+  const RecCfg rc = rec_cfg(st, wmax, grid, max_smem, ntiles);
+  if (rc.S <= 0) return 1;
+  if (wmax > 8)
+    return x_dtype == CCQ_DTYPE_BF16
+               ? launch_rec<2, CCQ_DTYPE_BF16, true>(st, x, wmax, y, x_dtype, y_dtype, grid, rc, s, offsets_dev, E, rows_e)
+               : launch_rec<2, CCQ_DTYPE_F16, true>(st, x, wmax, y, x_dtype, y_dtype, grid, rc, s, offsets_dev, E, rows_e);
+  return x_dtype == CCQ_DTYPE_BF16
+             ? launch_rec<1, CCQ_DTYPE_BF16, true>(st, x, wmax, y, x_dtype, y_dtype, grid, rc, s, offsets_dev, E, rows_e)
+             : launch_rec<1, CCQ_DTYPE_F16, true>(st, x, wmax, y, x_dtype, y_dtype, grid, rc, s, offsets_dev, E, rows_e);
 }
 
 int mma_min_tokens() {

@@ -111,6 +111,10 @@ extern "C" int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t
   }
   const int64_t T = offsets_host[E];
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  {  // decode batches: one tensor-pipe GEMV launch over the routed experts' tiles
+    const int st = launch_grouped_gemv(stack, E, re, offsets_device, offsets_host, T, x, x_dtype, y, y_dtype, s);
+    if (st != 1) return st;
+  }
   if (offsets_device && gemm_supported(stack, max_tokens))
     return launch_grouped_gemm(stack, E, re, offsets_device, T, max_tokens, x, x_dtype, y, y_dtype, s);
   // Other families: one fused decode-matmul per expert with tokens, on a

@@ -371,6 +371,29 @@ def test_experts_single_launch_matches_per_expert_oracle(oracle, ccq, cuda, fam,
     assert rel_err(y32.cpu().numpy(), want) < REL_TOL
 
 
+@pytest.mark.parametrize("counts", [[1, 0, 0, 1, 0, 1, 1, 0], [0, 0, 3, 0, 0, 0, 0, 0], [2, 2, 2, 2, 2, 2, 2, 2],
+                                    [1] * 8, [0, 16, 0, 0, 0, 0, 0, 0], [0, 0, 0, 0, 0, 0, 0, 1],
+                                    [9, 16, 0, 12, 5, 1, 0, 16]])
+@pytest.mark.parametrize("xdt", ["bf16", "f16"])
+def test_experts_decode_grouped_gemv(oracle, ccq, cuda, counts, xdt):
+    """Decode batches (<= 16 routed rows): one tensor-pipe GEMV launch over the
+    tiles of the experts that have tokens; experts without tokens are skipped."""
+    torch = cuda
+    E, rows, cols = 8, 48, 1024 + 64
+    secs, offs, x, want = _expert_case(oracle, 2, E, rows, cols, counts, seed=sum(counts) * 3 + 1)
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s_) for s_ in secs])
+    tdt = torch.bfloat16 if xdt == "bf16" else torch.float16
+    xt = torch.from_numpy(x).to("cuda").to(tdt)
+    y = ccq.experts_matmul(ex, offs, xt)
+    torch.cuda.synchronize()
+    want = np.zeros((int(offs[-1]), rows), np.float32)
+    xr = xt.float().cpu().numpy()
+    for e in range(E):
+        if counts[e]:
+            want[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], xr[offs[e]:offs[e + 1]], threads=8)
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
+
+
 def test_experts_one_launch_and_untouched_padding(oracle, ccq, cuda):
     torch = cuda
     counts = [3, 0, 40, 0, 9, 0, 0, 100]
