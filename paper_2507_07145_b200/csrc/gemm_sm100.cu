@@ -273,16 +273,20 @@ struct GF<kF25> {
   static constexpr int BOXB = 160, STAGES_C = 4, NIB = 0, SPLIT = 2;
 };
 
+// Ring shape: with kPar = 3 decode groups, SA = 2 * kPar stages lets a decode
+// group write a slot whose MMA finished a whole round ago instead of waiting
+// for the MMA it just fed (measured: the empty-slot wait dominated small-N
+// tiles, profiles/r01_ncu_gemm_M32.txt).  TMEM: SPLIT*BN + SA*G*SPLIT*32 <= 512.
 template <int FAM, int BN>
 constexpr int groups_per_stage() {
-  return GF<FAM>::SPLIT == 2 ? (BN <= 64 ? 2 : 1) : (BN <= 64 ? 4 : (BN <= 128 ? 2 : 1));
+  return GF<FAM>::SPLIT == 2 ? 1 : (BN <= 64 ? 2 : 1);
 }
-template <int BN>
-constexpr int stages_a() { return BN <= 64 ? 3 : 4; }
+template <int FAM, int BN>
+constexpr int stages_a() { return (GF<FAM>::SPLIT == 2 && BN > 64) || BN > 128 ? 4 : 6; }
 
 template <int FAM, int BN>
 struct GemmSmem {
-  static constexpr int SA = stages_a<BN>();
+  static constexpr int SA = stages_a<FAM, BN>();
   static constexpr int SB = SA;
   static constexpr int G = groups_per_stage<FAM, BN>();
   static constexpr int SC = GF<FAM>::STAGES_C;
