@@ -433,6 +433,14 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   const bool active = lane < ng;
 
   TRACE(0);
+#ifdef CCQ_GEMV_TRACE
+  if (lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const int gwid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gwid < 8192) g_trace[gwid * 16 + 12] = smid;
+  }
+#endif
   // 1. Barriers.  Activations arrive with ONE bulk copy per CTA (not one L2
   //    read per warp - all SMs read the same few lines of x, which hot-spots
   //    L2 slices).

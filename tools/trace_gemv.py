@@ -38,3 +38,16 @@ for i, n in enumerate(names):
 print("tiles per warp: min", t[:, 5].min(), "max", t[:, 5].max(), "mean", t[:, 5].mean())
 loop = rel[:, 9] - rel[:, 8]
 print(f"loop time per warp: p50 {np.median(loop):.2f} max {loop.max():.2f} us; per tile p50 {np.median(loop / np.maximum(t[:, 5], 1)):.3f} us")
+
+# per-CTA view: slowest warp loop end per CTA vs SM id (die locality / imbalance)
+wpc = 16
+nct = t.shape[0] // wpc
+cta_end = rel[: nct * wpc, 9].reshape(nct, wpc).max(1)
+cta_first = rel[: nct * wpc, 8].reshape(nct, wpc).min(1)
+smid = t[: nct * wpc, 12].reshape(nct, wpc)[:, 0]
+order = np.argsort(smid)
+print("CTA loop-end (max over warps) by SM id, us:")
+print(" ".join(f"{int(smid[i])}:{cta_end[i]:.1f}" for i in order))
+lo = smid < 74
+print(f"SM<74 mean end {cta_end[lo].mean():.2f} max {cta_end[lo].max():.2f}; SM>=74 mean {cta_end[~lo].mean():.2f} max {cta_end[~lo].max():.2f}")
+print(f"first data by SM half: {cta_first[lo].mean():.2f} / {cta_first[~lo].mean():.2f}")
