@@ -224,6 +224,10 @@ struct GemmArgs {
   int tpe;  // row tiles per expert
   int xs;   // activation rows per token (2 = f32 hi/lo split)
   const float* inv_scale;  // [tokens] power-of-two activation scale
+  // split-K (dense only): blockIdx.z owns K blocks [z*kbs, min((z+1)*kbs, nkb)),
+  // raw f32 partials go to partial[z][token][row] and a reduce kernel scales them
+  int kbs;
+  float* partial;
 };
 
 __device__ __forceinline__ uint32_t lop_mask_or(uint32_t v, uint32_t mask, uint32_t magic) {
@@ -458,7 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     y_ld = a.rows;
     y_col0 = 0;
   }
-  const int nkb = a.nkb;
+  const int kb0 = a.partial ? int(blockIdx.z) * a.kbs : 0;  // first (absolute) K block
+  const int nkb = a.partial ? min(a.kbs, a.nkb - kb0) : a.nkb;  // K blocks of this CTA
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SA; ++s) {
@@ -495,14 +500,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&full[s], uint32_t(ng) * SM::B_BLOCK);
         for (int gg = 0; gg < ng; ++gg)
           tma_load_2d(smem + SM::OFF_B + s * SM::B_BYTES + gg * SM::B_BLOCK, &tm_x,
-                      (st * G + gg) * kBK, n0 * a.xs, &full[s]);
+                      (kb0 + st * G + gg) * kBK, n0 * a.xs, &full[s]);
       }
     }
   } else if (warp == kWarpCodes) {
     if (lane == 0) {
       // ---------------- TMA producer: packed codes (runs ahead on its own ring) ----
       for (int cb = 0; cb * 8 < nkb; ++cb) {
-        const int kb = cb * 8, cs = cb % kStagesC;
+        const int kb = kb0 + cb * 8, cs = cb % kStagesC;
         mbar_wait(&code_empty[cs], ((cb / kStagesC) + 1) & 1);
         mbar_arrive_expect_tx(&code_full[cs], SM::C_BYTES + SM::N_BYTES);
         const int c = kb / kChunk, jb = (kb % kChunk) / 8;
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t h[32];
       uint32_t h2[SPLIT == 2 ? 32 : 1];
       if constexpr (FAM == kF206) {
-        const int jb = (kb % kChunk) / 8;
+        const int jb = ((kb0 + kb) % kChunk) / 8;
         uint32_t nibword;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
                      : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4)));
@@ -665,7 +670,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(fmaf(64.f, __uint_as_float(vh[i]), __uint_as_float(v[i])));
       }
       tmem_ld_wait();
-      if (row < row_end) {
+      if (row < row_end && a.partial) {
+        // split-K: raw sums (hi + lo parts for f32 inputs), scaled by the reduce kernel
+        float* pz = a.partial + size_t(blockIdx.z) * size_t(a.M) * size_t(a.rows);
+        const int per = 32 / a.xs;
+#pragma unroll 1
+        for (int i = 0; i < per; ++i) {
+          const int64_t n = n0 + (cc / a.xs) + i;
+          if (n < tok_end) {
+            const float v0 = a.xs == 1 ? __uint_as_float(v[i]) : __uint_as_float(v[2 * i]) + __uint_as_float(v[2 * i + 1]);
+            pz[n * a.rows + row] = v0;
+          }
+        }
+      } else if (row < row_end) {
         if (a.xs == 1) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -687,6 +704,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == kWarpMma) tmem_dealloc<kTmemCols>(tmem_d);
+}
+
+// Split-K epilogue: y[n][r] = (sum_z partial[z][n][r]) * super[r] * inv_scale[n],
+// summed in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ part, int splits, int64_t M,
+                                                     int64_t rows, const float* __restrict__ super,
+                                                     const float* __restrict__ inv_scale, void* y, int y_dtype) {
+  const int64_t total = M * rows;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += part[size_t(z) * size_t(total) + size_t(i)];
+    const int64_t n = i / rows, r = i - n * rows;
+    v *= super[r] * inv_scale[n];
+    if (y_dtype == CCQ_DTYPE_F32)
+      static_cast<float*>(y)[i] = v;
+    else
+      static_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn(v);
+  }
 }
 
 template <int FAM, int BN>
@@ -727,7 +762,7 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
     return st;
   }
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
-             offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale};
+             offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr};
   auto kern = gemm_ccq<FAM, BN>;
   static bool configured[5] = {};
   if (!configured[BN / 64]) {
@@ -735,13 +770,45 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
     configured[BN / 64] = true;
   }
   const int tb = BN / xs;
-  const dim3 grid = grouped ? dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe))
-                            : dim3(unsigned((M + tb - 1) / tb), unsigned((m->rows + kBM - 1) / kBM));
+  dim3 grid = grouped ? dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe))
+                      : dim3(unsigned((M + tb - 1) / tb), unsigned((m->rows + kBM - 1) / kBM));
+  // Split K when the tiles would leave most SMs idle (K-heavy shapes such as
+  // 14336 -> 4096: 32 row tiles); splits cover whole 8-group code blocks.
+  float* part = nullptr;
+  int splits = 1;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = int64_t(grid.x) * grid.y;
+    const int cblocks = int((m->gpr + 7) / 8);
+    if (!grouped && tiles > 0 && tiles * 2 <= sms && cblocks >= 8) {
+      splits = int(std::min<int64_t>(sms / tiles, cblocks / 4));
+      if (splits >= 2) {
+        const int cb_per = (cblocks + splits - 1) / splits;
+        a.kbs = cb_per * 8;
+        splits = (cblocks + cb_per - 1) / cb_per;
+        CCQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(splits) * size_t(M) * size_t(m->rows) * 4, s));
+        a.partial = part;
+        grid.z = unsigned(splits);
+      } else {
+        splits = 1;
+      }
+    }
+  }
   if (grid.x && grid.y) {
     kern<<<grid, kThreads, SM::TOTAL, s>>>(tm_codes, tm_nib, tm_x, a);
     count_launch();
+    if (part) {
+      const int64_t total = M * m->rows;
+      const unsigned blocks = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 8));
+      splitk_reduce<<<blocks, 256, 0, s>>>(part, splits, M, m->rows, m->super, inv_scale, y, y_dtype);
+      count_launch();
+    }
   }
   cudaError_t e = cudaGetLastError();
+  if (part) cudaFreeAsync(part, s);
   cudaFreeAsync(x16, s);
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemm launch");
 }

@@ -287,7 +287,8 @@ def test_baseline_shape_full_size(oracle, ccq, cuda, fam):
 # ------------------------------------------------------------ gemm (c) tcgen05 --
 
 @pytest.mark.parametrize("fam", [0, 1, 2])
-@pytest.mark.parametrize("shape", [(128, 512), (200, 4096), (384, 2048 + 64), (130, 14336), (64, 192)])
+@pytest.mark.parametrize("shape", [(128, 512), (200, 4096), (384, 2048 + 64), (130, 14336), (64, 192),
+                                   (1000, 8192 + 512)])
 @pytest.mark.parametrize("M", [9, 32, 64, 100, 128, 256, 300])
 def test_gemm_tcgen05_bf16(oracle, ccq, cuda, fam, shape, M):
     """All three families on tcgen05: exact f16 weight operands (2.5 as two
