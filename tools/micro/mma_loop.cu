@@ -7,7 +7,7 @@
 #include "../../paper_2507_07145_b200/csrc/tcgen05.cuh"
 using namespace ccqb;
 
-template <int V>
+template <int V, int N = 64>
 __global__ void bench(unsigned long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, cbar[16];
@@ -23,7 +23,7 @@ __global__ void bench(unsigned long long* out, int iters) {
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
     mbar_arrive(&bar);  // complete phase 0 of `bar`
-    const uint32_t idesc = idesc_f16_f32(128, 64);
+    const uint32_t idesc = idesc_f16_f32(128, N);
     const uint32_t b = smem_addr(smem);
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
@@ -41,18 +41,20 @@ __global__ void bench(unsigned long long* out, int iters) {
   if (warp == 0) tmem_dealloc<512>(tm);
 }
 
-template <int V>
+template <int V, int N = 64>
 void run(unsigned long long* d) {
-  auto k = bench<V>;
+  auto k = bench<V, N>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
   k<<<1, 128, 100000>>>(d, 1024);
   cudaDeviceSynchronize();
   unsigned long long h;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("variant %d: %.1f cycles per K block (4 MMA N=64)  %s\n", V, h / 1024.0, cudaGetErrorString(cudaGetLastError()));
+  printf("variant %d N=%3d: %.1f cycles per K block (4 MMA)  %s\n", V, N, h / 1024.0, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 64);
   run<0>(d); run<1>(d); run<2>(d);
+  run<2, 16>(d); run<2, 32>(d); run<2, 128>(d); run<2, 256>(d);
+  run<0, 16>(d); run<0, 32>(d); run<0, 256>(d);
 }
