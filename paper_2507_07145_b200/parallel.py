@@ -58,3 +58,55 @@ class ShardedLinear:
         from . import matmul
         y_local = matmul(self.local, x, out_dtype=out_dtype)
         return gather_row_blocks(y_local, self.rows, self.group)
+
+
+def gather_token_blocks(y_local: torch.Tensor, counts, group=None) -> torch.Tensor:
+    """All-gather per-rank blocks of consecutive output rows ([counts[r], N]
+    on rank r, counts known to every rank) into the concatenated [sum, N]."""
+    world = dist.get_world_size(group)
+    cmax = max(int(c) for c in counts) if counts else 0
+    n = y_local.shape[1]
+    buf = torch.zeros(max(cmax, 1), n, dtype=y_local.dtype, device=y_local.device)
+    if y_local.shape[0]:
+        buf[: y_local.shape[0]] = y_local
+    out = torch.empty(world, max(cmax, 1), n, dtype=y_local.dtype, device=y_local.device)
+    if hasattr(dist, "all_gather_into_tensor") and y_local.is_cuda:
+        dist.all_gather_into_tensor(out, buf.contiguous(), group=group)
+    else:
+        parts = list(out.unbind(0))
+        dist.all_gather(parts, buf.contiguous(), group=group)
+        out = torch.stack(parts)
+    return torch.cat([out[r, : int(counts[r])] for r in range(world)], dim=0)
+
+
+class ShardedExperts:
+    """An MoE layer whose experts are split across the ranks of `group`
+    (SURVEY 8e): rank p holds experts [p*E/P, (p+1)*E/P) as one stacked device
+    model, computes the expert-major output rows of its experts for the routed
+    tokens, and the full output is formed by ONE all-gather."""
+
+    def __init__(self, packed_experts, device: int, group=None):
+        from . import Experts
+        self.group = group
+        self.E = len(packed_experts)
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        self.e0, self.e1 = block_range(self.E, rank, world)
+        self.world = world
+        self.rows_e = packed_experts[0].rows
+        self.local = Experts.upload(packed_experts[self.e0:self.e1], device=device) if self.e1 > self.e0 else None
+
+    def __call__(self, offsets, x: torch.Tensor, out_dtype=torch.float32) -> torch.Tensor:
+        """offsets: E+1 host ints (expert-major token layout of x, all experts)."""
+        import numpy as np
+        from . import experts_matmul
+        offs = np.asarray(offsets, np.int64)
+        counts = [int(offs[block_range(self.E, r, self.world)[1]] - offs[block_range(self.E, r, self.world)[0]])
+                  for r in range(self.world)]
+        lo, hi = int(offs[self.e0]), int(offs[self.e1])
+        if self.local is not None and hi > lo:
+            local_offs = (offs[self.e0:self.e1 + 1] - lo).astype(np.int32)
+            y_local = experts_matmul(self.local, local_offs, x[lo:hi].contiguous(), out_dtype=out_dtype)
+        else:
+            y_local = torch.empty(0, self.rows_e, dtype=out_dtype, device=x.device)
+        return gather_token_blocks(y_local, counts, self.group)

@@ -81,3 +81,72 @@ def test_block_ranges_cover_exactly():
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def _expert_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    from paper_2507_07145_b200.parallel import block_range, gather_token_blocks
+    E, rows, cols = 5, 24, 128
+    secs = [O.random_packed(rows, cols, 2, 64, seed=e) for e in range(E)]
+    counts = [2, 0, 3, 1, 4]
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    x = O.random_matrix(int(offs[-1]), cols, "gaussian", 3)
+    e0, e1 = block_range(E, rank, world)
+    blocks = [O.gemv_batch(secs[e], x[offs[e]:offs[e + 1]]) for e in range(e0, e1) if counts[e]]
+    y_local = torch.from_numpy(np.concatenate(blocks) if blocks else np.zeros((0, rows), np.float32))
+    per_rank = [int(offs[block_range(E, r, world)[1]] - offs[block_range(E, r, world)[0]]) for r in range(world)]
+    y = gather_token_blocks(y_local, per_rank)
+    if rank == 0:
+        q.put(y.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_expert_sharded_gather_equals_unsharded():
+    """Experts split over 2 ranks (3 + 2), variable routed-token counts per
+    rank: the gathered expert-major output equals the unsharded one."""
+    import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_expert_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    E, rows, cols = 5, 24, 128
+    secs = [O.random_packed(rows, cols, 2, 64, seed=e) for e in range(E)]
+    counts = [2, 0, 3, 1, 4]
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    x = O.random_matrix(int(offs[-1]), cols, "gaussian", 3)
+    want = np.concatenate([O.gemv_batch(secs[e], x[offs[e]:offs[e + 1]]) for e in range(E) if counts[e]])
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_sharded_linear_and_experts_nccl_world1():
+    """The NCCL path on the GPU (world size 1 in-process): ShardedLinear and
+    ShardedExperts equal the unsharded kernels bit for bit."""
+    import paper_2507_07145_b200 as P
+    from paper_2507_07145_b200.parallel import ShardedExperts, ShardedLinear
+    from paper_2507_07145_b200.synthetic import random_packed
+    port = _free_port()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        pk = random_packed(300, 1024, 2, 64, 5)
+        x = torch.randn(3, 1024, device="cuda").to(torch.bfloat16)
+        lin = ShardedLinear(pk, device=0)
+        ref = P.matmul(P.DeviceModel.upload(pk), x)
+        assert torch.equal(lin(x), ref)
+        exps = [random_packed(48, 1024, 2, 64, 10 + e) for e in range(4)]
+        offs = [0, 1, 1, 3, 4]
+        xe = torch.randn(4, 1024, device="cuda").to(torch.bfloat16)
+        got = ShardedExperts(exps, device=0)(offs, xe)
+        want = P.experts_matmul(P.Experts.upload(exps), offs, xe)
+        assert torch.equal(got, want)
+    finally:
+        dist.destroy_process_group()
