@@ -277,16 +277,18 @@ struct GF<kF25> {
   static constexpr int BOXB = 160, STAGES_C = 4, NIB = 0, SPLIT = 2;
 };
 
-// Ring shape: with kPar = 3 decode groups, SA = 2 * kPar stages lets a decode
-// group write a slot whose MMA finished a whole round ago instead of waiting
-// for the MMA it just fed (measured: the empty-slot wait dominated small-N
-// tiles, profiles/r01_ncu_gemm_M32.txt).  TMEM: SPLIT*BN + SA*G*SPLIT*32 <= 512.
+// Ring shape.  Each stage holds G groups (K = 64 G): the MMA issuer pays one
+// mbarrier wait + fence + commit per stage (~250 cycles,
+// profiles/r01_micro_tcgen05_issue.txt), so small-N tiles batch several
+// groups per stage.  (Measured: a deeper 2*kPar-stage ring with G = 2 did not
+// help small M and slowed the grouped MoE GEMM by 15 %.)
+// TMEM: SPLIT*BN + SA*G*SPLIT*32 <= 512.
 template <int FAM, int BN>
 constexpr int groups_per_stage() {
-  return GF<FAM>::SPLIT == 2 ? 1 : (BN <= 64 ? 2 : 1);
+  return GF<FAM>::SPLIT == 2 ? (BN <= 64 ? 2 : 1) : (BN <= 64 ? 4 : (BN <= 128 ? 2 : 1));
 }
 template <int FAM, int BN>
-constexpr int stages_a() { return (GF<FAM>::SPLIT == 2 && BN > 64) || BN > 128 ? 4 : 6; }
+constexpr int stages_a() { return BN <= 64 ? 3 : 4; }
 
 template <int FAM, int BN>
 struct GemmSmem {
