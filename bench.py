@@ -31,6 +31,13 @@ sys.path.insert(0, ROOT)
 METRIC = "CCQ W2A16 GEMV packed-weight GB/s (% HBM peak); GEMM TFLOP/s at batch 1-256"
 D_IN, D_OUT, FAMILY, M_HEAD = 4096, 14336, 2, 1
 SEED = 4096 * 31 + 14336  # ccq_main.cpp:269-271 seeding: seed + d_in*31 + d_out (seed 0)
+WORKLOAD = "configs[1] Llama-3-8B MLP-up linear d_in 4096 -> d_out 14336, CCQ 2.06 (W2A16), batch M=1"
+
+
+def base_config(layers):
+    """The workload description shared by both arms (same keys, same values)."""
+    return {"workload": WORKLOAD, "d_in": D_IN, "d_out": D_OUT, "family": "2.06", "batch": M_HEAD,
+            "layers_per_step": layers}
 
 
 def load_peaks():
@@ -124,8 +131,7 @@ def run_reference(args, world, rank):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (random_quantized, Gaussian x)",
-            "config": {"workload": "configs[1] Llama-3-8B MLP-up linear 4096->14336, CCQ 2.06, M=1",
-                       "d_in": D_IN, "d_out": D_OUT, "family": "2.06", "batch": M_HEAD},
+            "config": dict(base_config(args.layers), parallelism="reference CPU path, host threads"),
             "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
                              "sample": sample},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -303,13 +309,10 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic: random_quantized CCQ 2.06 weights (synthetic.cpp:25-103), "
                     "Gaussian bf16 activations",
-            "config": {"workload": "configs[1] Llama-3-8B MLP-up linear d_in 4096 -> d_out 14336, "
-                                   "CCQ 2.06 (W2A16), batch M=1",
-                       "d_in": D_IN, "d_out": D_OUT, "family": "2.06", "batch": M_HEAD,
-                       "layers_per_step": args.layers,
-                       "l2": f"inputs larger than L2: {args.layers} resident layer copies = "
-                             f"{bytes_step/1e6:.0f} MB rotated per step",
-                       "parallelism": f"replicas x{world}"},
+            "config": dict(base_config(args.layers),
+                           l2=f"inputs larger than L2: {args.layers} resident layer copies = "
+                              f"{bytes_step/1e6:.0f} MB rotated per step",
+                           parallelism=f"replicas x{world}"),
             "hbm_fraction": value / world / hbm_peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
