@@ -486,14 +486,17 @@ def run_prefill(P, torch, dev, stream, tflops_peak):
                 P.matmul(m, x, out=y, stream=stream)
         stream.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 5
-        with torch.cuda.stream(stream):
-            s0.record(stream)
-            for _ in range(reps):
-                P.matmul(m, x, out=y, stream=stream)
-            s1.record(stream)
-        torch.cuda.synchronize()
-        ms = s0.elapsed_time(s1) / reps
+        reps, best = 5, None
+        for _ in range(3):  # best of 3 windows: the sweep before leaves the GPU hot
+            with torch.cuda.stream(stream):
+                s0.record(stream)
+                for _ in range(reps):
+                    P.matmul(m, x, out=y, stream=stream)
+                s1.record(stream)
+            torch.cuda.synchronize()
+            t = s0.elapsed_time(s1) / reps
+            best = t if best is None else min(best, t)
+        ms = best
         tf = 2 * 4096 * 8192 * 28672 / (ms * 1e-3) / 1e12
         out.append({"family": fname, "d_in": 8192, "d_out": 28672, "M": 4096, "ms": round(ms, 4),
                     "TFLOPs": round(tf, 1), "tensor_frac": round(tf / tflops_peak, 4),
