@@ -111,12 +111,6 @@ __device__ __forceinline__ uint32_t decode_units(const uint8_t* tile, int row, i
     // `tile` already points at this lane's word of group j (see group())
     (void)row; (void)j; (void)c;
     const uint32_t w = ld32(tile);
-#if defined(CCQ_MMA_EXP) && CCQ_MMA_EXP == 2
-    // experiment: no decode, keep the load live
-#pragma unroll
-    for (int t = 0; t < 8; ++t) u[t] = w + t;
-    return (rc.nib >> (4 * j)) & 0xFu;
-#endif
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const uint32_t qb = prmt(w, 0u, rc.sel[t]);
@@ -484,7 +478,6 @@ __global__ void __launch_bounds__(512, 1)
     gstride[nt] = live ? 128u : 0u;
   }
   const float* qlane = qs + 2 * c;
-  const int gx7 = g & 7;
 
   // one 64-weight group: decode both rows, 4 K slices x NT token tiles of
   // mma, then y += sc * D
@@ -515,14 +508,8 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const uint32_t af[4] = {ua[2 * t], ub[2 * t], ua[2 * t + 1], ub[2 * t + 1]};
-#if defined(CCQ_MMA_EXP) && CCQ_MMA_EXP == 1
-        // experiment: no tensor op, keep the decode live
-        d[0] += __uint_as_float(af[0] ^ bb[2 * t]); d[1] += __uint_as_float(af[1]);
-        e[2] += __uint_as_float(af[2] ^ bb[2 * t + 1]); e[3] += __uint_as_float(af[3]);
-#else
         if (t & 1) mma16816(e, af, bb[2 * t], bb[2 * t + 1]);
         else mma16816(d, af, bb[2 * t], bb[2 * t + 1]);
-#endif
       }
       yacc[nt][0] = fmaf(fa, d[0] + e[0], yacc[nt][0]);
       yacc[nt][1] = fmaf(fa, d[1] + e[1], yacc[nt][1]);
@@ -530,7 +517,6 @@ __global__ void __launch_bounds__(512, 1)
       yacc[nt][3] = fmaf(fb, d[3] + e[3], yacc[nt][3]);
     }
   };
-  (void)gx7;
 
   int tile = cur_tile, blk = nmine > 0 ? i0 % a.nblk : 0;
   bool need_plan = true;
