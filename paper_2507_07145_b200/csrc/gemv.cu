@@ -841,11 +841,13 @@ int num_sms(int device) {
   return cached[device];
 }
 
-// Dispatch (measured, profiles/): the CUDA-core streaming GEMV wins at M = 1;
-// from M = 2 the tcgen05 GEMM is faster where it exists (2.06).
+// Dispatch (measured, profiles/r01_sweep.json): the CUDA-core streaming GEMV
+// takes M = 1.
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
+  // M = 1 only: batches go to the tensor-pipe GEMV (when their activations
+  // fit one launch) or to the tcgen05 GEMM (profiles/r01_sweep.json)
   if (m->geo.group_size != 64 || m->nch > 16) return false;
-  return m->family == kF206 ? M <= 1 : M <= 8;
+  return M <= 1;
 }
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
