@@ -354,7 +354,7 @@ __device__ __forceinline__ void stage_activations(const MmaArgs& a, uint8_t* xs,
   __syncthreads();
 }
 
-template <int FAM, int NT, int S, int XDT, bool P2>
+template <int FAM, int NT, int S, int XDT, bool P2, bool GROUPED = false>
 __global__ void __launch_bounds__(512, 1)
     gemv_mma(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_side,
              MmaArgs a) {
@@ -386,10 +386,56 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* xbar = bars + nw * S;
   uint8_t* ring = rings + size_t(warp) * S * STAGE;
 
-  // CTA tiles and this warp's item range (tile-major items of 8-group blocks)
-  const int t_begin = int(int64_t(blockIdx.x) * a.ntiles / gridDim.x);
-  const int t_end = int(int64_t(blockIdx.x + 1) * a.ntiles / gridDim.x);
+  // grouped experts: compact the experts that have tokens; their tiles are the work
+  __shared__ int hit[256];
+  __shared__ int nhit_s, wsum[16];
+  int ntiles = a.ntiles;
+  const int tpe = GROUPED ? int(a.rows_e / kRowsT) : 1;
+  if constexpr (GROUPED) {
+    const int e = threadIdx.x;
+    const bool has = e < a.E && a.offsets[e + 1] > a.offsets[e];
+    const unsigned bal = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < nw; ++w) { const int t = wsum[w]; wsum[w] = acc; acc += t; }
+      nhit_s = acc;
+    }
+    __syncthreads();
+    if (has) hit[wsum[warp] + __popc(bal & ((1u << lane) - 1u))] = e;
+    __syncthreads();
+    ntiles = nhit_s * tpe;
+  }
+  // tile -> stack row of its first row, token range (expert-major x / y)
+  auto tile_info = [&](int t, int64_t& row0, int& off, int& cnt) {
+    if constexpr (GROUPED) {
+      const int e = hit[t / tpe];
+      row0 = int64_t(e) * a.rows_e + int64_t(t % tpe) * kRowsT;
+      off = a.offsets[e];
+      cnt = a.offsets[e + 1] - off;
+    } else {
+      row0 = int64_t(t) * kRowsT;
+      off = 0;
+      cnt = a.M;
+    }
+  };
+  // CTA tiles and this warp's item range (tile-major items of K blocks)
+  const int t_begin = int(int64_t(blockIdx.x) * ntiles / gridDim.x);
+  const int t_end = int(int64_t(blockIdx.x + 1) * ntiles / gridDim.x);
   const int nitems = (t_end - t_begin) * a.nblk;
+  int tok0 = 0, Mc = M;  // staged token window
+  if constexpr (GROUPED) {
+    Mc = 0;
+    if (t_end > t_begin) {
+      int64_t r0;
+      int o0, c0, o1, c1;
+      tile_info(t_begin, r0, o0, c0);
+      tile_info(t_end - 1, r0, o1, c1);
+      tok0 = o0;
+      Mc = o1 + c1 - o0;
+    }
+  }
   const int i0 = int(int64_t(warp) * nitems / nw), i1 = int(int64_t(warp + 1) * nitems / nw);
   const int nmine = i1 - i0;
 
@@ -414,7 +460,10 @@ __global__ void __launch_bounds__(512, 1)
     if (lane == 0 && k < nmine) {
       constexpr int BPC = kChunk / F::BLK;  // blocks per 32-group chunk
       const int chunk = iss_blk / BPC;
-      const int ycoord = int(int64_t(chunk) * a.rows_pad + int64_t(iss_tile) * kRowsT);
+      int64_t row0;
+      int toff_, tcnt_;
+      tile_info(iss_tile, row0, toff_, tcnt_);
+      const int ycoord = int(int64_t(chunk) * a.rows_pad + row0);
       uint8_t* st = ring + (k % S) * STAGE;
       mbar_arrive_expect_tx(&mybar[k % S], uint32_t(CODE_B + SIDE_B));
       tma_load_2d(st, &tm_codes, (iss_blk - chunk * BPC) * F::BOX, ycoord, &mybar[k % S]);
@@ -439,7 +488,7 @@ __global__ void __launch_bounds__(512, 1)
 
   const uint32_t row_bytes = uint32_t(gpr) * 128u;
   const uint32_t tok_stride = row_bytes + 16u;  // +16 B: tokens land in different banks
-  stage_activations<FAM, MP, XDT>(a, xs, qs, tokscale, tokmax, M, gpr, lane);
+  stage_activations<FAM, MP, XDT>(a, xs, qs, tokscale, tokmax, Mc, gpr, lane, tok0);
 #ifdef CCQ_GEMV_TRACE
   MTRACE(3, gtime());
   MTRACE(7, nmine);
@@ -470,14 +519,24 @@ __global__ void __launch_bounds__(512, 1)
   const uint8_t* xb[NT];
   uint32_t gstride[NT];
   uint8_t* zblk = reinterpret_cast<uint8_t*>(wrange + 32);  // 128 B of zeros
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int nb = nt * 8 + g;
-    const bool live = nb < M;
-    xb[nt] = live ? xs + size_t(nb) * tok_stride + c * 32 : zblk + c * 32;
-    gstride[nt] = live ? 128u : 0u;
-  }
   const float* qlane = qs + 2 * c;
+  // B operand rows and -Q columns of a tile's tokens (grouped: the tile's
+  // expert, as rows of the staged window)
+  auto set_tokens = [&](int tile_abs) {
+    int64_t r0;
+    int toff, tcnt;
+    tile_info(tile_abs, r0, toff, tcnt);
+    toff -= tok0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int nb = nt * 8 + g;
+      const bool live = nb < tcnt;
+      xb[nt] = live ? xs + size_t(toff + nb) * tok_stride + c * 32 : zblk + c * 32;
+      gstride[nt] = live ? 128u : 0u;
+    }
+    qlane = qs + toff + 2 * c;
+  };
+  if (nmine > 0) set_tokens(t_begin + i0 / a.nblk);
 
   // one 64-weight group: decode both rows, 4 K slices x NT token tiles of
   // mma, then y += sc * D
@@ -497,8 +556,16 @@ __global__ void __launch_bounds__(512, 1)
     const float fa = float(sca), fb = float(scb);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const float2 q2 = *reinterpret_cast<const float2*>(qlane + G * MP + nt * 8);
-      float d[4] = {q2.x, q2.y, q2.x, q2.y};
+      float q0, q1;
+      if constexpr (GROUPED) {  // odd token offsets: scalar loads
+        q0 = qlane[G * MP + nt * 8];
+        q1 = qlane[G * MP + nt * 8 + 1];
+      } else {
+        const float2 q2 = *reinterpret_cast<const float2*>(qlane + G * MP + nt * 8);
+        q0 = q2.x;
+        q1 = q2.y;
+      }
+      float d[4] = {q0, q1, q0, q1};
       const uint4* src = reinterpret_cast<const uint4*>(xb[nt] + uint32_t(G) * gstride[nt]);
       const uint4 b01 = src[0], b23 = src[1];
       const uint32_t bb[8] = {b01.x, b01.y, b01.z, b01.w, b23.x, b23.y, b23.z, b23.w};
@@ -526,6 +593,7 @@ __global__ void __launch_bounds__(512, 1)
       flush(cur_tile);
       cur_tile = tile;
       need_plan = true;
+      if constexpr (GROUPED) set_tokens(t_begin + tile);
     }
     const int s = k % S;
     mbar_wait(&mybar[s], uint32_t((k / S) & 1));
@@ -587,21 +655,25 @@ __global__ void __launch_bounds__(512, 1)
 
   // ---- per-tile sums in warp order, scaled by super and the token scale ----
   const int ntl = t_end - t_begin;
-  for (int e = threadIdx.x; e < ntl * kRowsT * M; e += blockDim.x) {
-    const int tl = e / (kRowsT * M), rem = e % (kRowsT * M);
-    const int r = rem / M, n = rem % M;
-    const int64_t row = int64_t(t_begin + tl) * kRowsT + r;
-    if (row >= a.rows) continue;
+  for (int e = threadIdx.x; e < ntl * kRowsT * MP; e += blockDim.x) {
+    const int tl = e / (kRowsT * MP), rem = e % (kRowsT * MP);
+    const int r = rem / MP, n = rem % MP;
+    int64_t row0;
+    int toff, tcnt;
+    tile_info(t_begin + tl, row0, toff, tcnt);
+    const int64_t row = row0 + r;
+    if (n >= tcnt || row >= a.rows) continue;
     float v = 0.f;
     for (int w = 0; w < nw; ++w) {
       const int ft = wrange[2 * w], lt = wrange[2 * w + 1];
       if (tl >= ft && tl <= lt) v += part[((size_t(w) * a.slots + (tl - ft)) * kRowsT + r) * MP + n];
     }
-    v *= a.super[row] * tokscale[n];
+    v *= a.super[row] * tokscale[toff - tok0 + n];
+    const int64_t yi = GROUPED ? int64_t(toff + n) * a.rows_e + (row % a.rows_e) : int64_t(n) * a.y_ld + row;
     if (a.y_dtype == CCQ_DTYPE_F32)
-      static_cast<float*>(a.y)[int64_t(n) * a.y_ld + row] = v;
+      static_cast<float*>(a.y)[yi] = v;
     else
-      static_cast<__nv_bfloat16*>(a.y)[int64_t(n) * a.y_ld + row] = __float2bfloat16_rn(v);
+      static_cast<__nv_bfloat16*>(a.y)[yi] = __float2bfloat16_rn(v);
   }
 #ifdef CCQ_GEMV_TRACE
   MTRACE(6, gtime());
@@ -918,11 +990,12 @@ struct Cfg {
 };
 
 template <int FAM, int NT, int S>
-Cfg plan_cfg(const ccq_dev_model* m, int M, int grid, int max_smem) {
+Cfg plan_cfg(const ccq_dev_model* m, int M, int grid, int max_smem, int ntiles_override = -1) {
   using F = MF<FAM>;
   constexpr int MP = 8 * NT;
   constexpr int STAGE = ((kRowsT * F::BOX + kRowsT * F::SIDE) + 511) & ~511;
-  const int ntiles = int((m->rows + kRowsT - 1) / kRowsT);
+  max_smem -= 2048;  // static shared memory (grouped expert list)
+  const int ntiles = ntiles_override >= 0 ? ntiles_override : int((m->rows + kRowsT - 1) / kRowsT);
   const int nblk = int((m->gpr + F::BLK - 1) / F::BLK);
   const int tiles_cta = (ntiles + grid - 1) / grid;
   static const int env_w = std::getenv("CCQ_MMA_WARPS") ? std::atoi(std::getenv("CCQ_MMA_WARPS")) : 0;
@@ -937,9 +1010,10 @@ Cfg plan_cfg(const ccq_dev_model* m, int M, int grid, int max_smem) {
   return Cfg{0, 0, 0};
 }
 
-template <int FAM, int NT, int S, int XDT, bool P2>
+template <int FAM, int NT, int S, int XDT, bool P2, bool GROUPED = false>
 int launch_chunk(const ccq_dev_model* m, const CUtensorMap& tmc, const CUtensorMap& tms, const void* x,
-                 int M, void* y, int x_dtype, int y_dtype, int grid, const Cfg& cfg, cudaStream_t s) {
+                 int M, void* y, int x_dtype, int y_dtype, int grid, const Cfg& cfg, cudaStream_t s,
+                 const int32_t* offsets = nullptr, int E = 0, int64_t rows_e = 0) {
   MmaArgs a{};
   a.super = m->super;
   a.plan = m->plan;
@@ -957,7 +1031,10 @@ int launch_chunk(const ccq_dev_model* m, const CUtensorMap& tmc, const CUtensorM
   a.x_ld = m->cols;
   a.y_ld = m->rows;
   a.xs_bytes = uint32_t((m->gpr * 128 + 16) * M);
-  auto kern = gemv_mma<FAM, NT, S, XDT, P2>;
+  a.offsets = offsets;
+  a.E = E;
+  a.rows_e = rows_e;
+  auto kern = gemv_mma<FAM, NT, S, XDT, P2, GROUPED>;
   static size_t configured[3][3][2] = {};
   size_t& conf = configured[NT][XDT][P2 ? 1 : 0];
   if (conf < cfg.smem) {
@@ -1052,17 +1129,53 @@ bool gemv_mma_fits(const ccq_dev_model* m, int64_t M) {
   return cfg.warps >= 8;
 }
 
+// Grouped experts on the TMA-box tensor-pipe GEMV (any family; partial sums
+// are O(warps), so any number of routed tiles fits).
+template <int FAM, bool P2>
+int launch_grouped_box(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev, int ntiles,
+                       int wmax, const void* x, int x_dtype, void* y, int y_dtype, cudaStream_t s) {
+  using F = MF<FAM>;
+  constexpr int S = 4;
+  CUtensorMap tmc{}, tms{};
+  int rc = make_map_2d(&tmc, CU_TENSOR_MAP_DATA_TYPE_UINT8, st->codes, st->rec, uint64_t(st->nch) * st->rows_pad,
+                       st->rec, F::BOX, kRowsT, FAM == kF206 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (rc != CCQ_OK) return rc;
+  if constexpr (F::SIDE > 0) {
+    rc = make_map_2d(&tms, CU_TENSOR_MAP_DATA_TYPE_UINT8, st->codes + st->cgb, F::SIDE,
+                     uint64_t(st->nch) * st->rows_pad, st->rec, F::SIDE, kRowsT, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc != CCQ_OK) return rc;
+  } else {
+    tms = tmc;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int grid = std::min(num_sms(dev), ntiles);
+  const Cfg cfg = wmax > 8 ? plan_cfg<FAM, 2, S>(st, wmax, grid, max_smem, ntiles)
+                           : plan_cfg<FAM, 1, S>(st, wmax, grid, max_smem, ntiles);
+  if (cfg.warps < 8) return 1;  // the expert compaction needs >= 256 threads
+  if (wmax > 8)
+    return x_dtype == CCQ_DTYPE_BF16
+               ? launch_chunk<FAM, 2, S, CCQ_DTYPE_BF16, P2, true>(st, tmc, tms, x, wmax, y, x_dtype, y_dtype, grid, cfg, s, offsets_dev, E, rows_e)
+               : launch_chunk<FAM, 2, S, CCQ_DTYPE_F16, P2, true>(st, tmc, tms, x, wmax, y, x_dtype, y_dtype, grid, cfg, s, offsets_dev, E, rows_e);
+  return x_dtype == CCQ_DTYPE_BF16
+             ? launch_chunk<FAM, 1, S, CCQ_DTYPE_BF16, P2, true>(st, tmc, tms, x, wmax, y, x_dtype, y_dtype, grid, cfg, s, offsets_dev, E, rows_e)
+             : launch_chunk<FAM, 1, S, CCQ_DTYPE_F16, P2, true>(st, tmc, tms, x, wmax, y, x_dtype, y_dtype, grid, cfg, s, offsets_dev, E, rows_e);
+}
+
 // Kernel (d) for decode batches: all routed (expert, token) rows in ONE
 // tensor-pipe GEMV launch over the tiles of the experts that have tokens.
 // Returns 1 when not applicable (caller falls back to the grouped GEMM).
 int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev,
                         const int32_t* offsets_host, int64_t T, const void* x, int x_dtype, void* y,
                         int y_dtype, cudaStream_t s) {
-  if (st->family != kF206 || st->plan_pos_min < 1 || T < 1 || E > 256 || rows_e % kRowsT != 0 ||
-      st->geo.group_size != 64 || st->cols % 64 != 0 || st->rec != uint32_t(st->cgb + 32) ||
+  if (T < 1 || E > 256 || rows_e % kRowsT != 0 || st->geo.group_size != 64 || st->cols % 64 != 0 ||
       x_dtype == CCQ_DTYPE_F32 || (reinterpret_cast<uintptr_t>(x) & 15u) || !offsets_dev ||
       std::getenv("CCQ_NO_GROUPED_GEMV"))
     return 1;
+  const bool rec_ok = st->family == kF206 && st->plan_pos_min >= 1 && st->rec == uint32_t(st->cgb + 32) &&
+                      !std::getenv("CCQ_NO_REC");
   int nhit = 0;
   for (int e = 0; e < E; ++e) nhit += offsets_host[e + 1] > offsets_host[e] ? 1 : 0;
   if (nhit == 0) return CCQ_OK;
@@ -1085,8 +1198,17 @@ int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const in
     wmax = std::max(wmax, offsets_host[e1 + 1] - offsets_host[e0]);
   }
   if (wmax > 16) return 1;  // some expert (or CTA window) has too many tokens: grouped GEMM
-  const RecCfg rc = rec_cfg(st, wmax, grid, max_smem, ntiles);
-  if (rc.S <= 0) return 1;
+  const RecCfg rc = rec_ok ? rec_cfg(st, wmax, grid, max_smem, ntiles) : RecCfg{0, 0};
+  if (rc.S <= 0) {
+    switch (st->family) {
+      case kF275: return launch_grouped_box<kF275, false>(st, E, rows_e, offsets_dev, ntiles, wmax, x, x_dtype, y, y_dtype, s);
+      case kF25: return launch_grouped_box<kF25, false>(st, E, rows_e, offsets_dev, ntiles, wmax, x, x_dtype, y, y_dtype, s);
+      default:
+        return st->plan_pos_min >= 1
+                   ? launch_grouped_box<kF206, true>(st, E, rows_e, offsets_dev, ntiles, wmax, x, x_dtype, y, y_dtype, s)
+                   : launch_grouped_box<kF206, false>(st, E, rows_e, offsets_dev, ntiles, wmax, x, x_dtype, y, y_dtype, s);
+    }
+  }
   if (wmax > 8)
     return x_dtype == CCQ_DTYPE_BF16
                ? launch_rec<2, CCQ_DTYPE_BF16, true>(st, x, wmax, y, x_dtype, y_dtype, grid, rc, s, offsets_dev, E, rows_e)

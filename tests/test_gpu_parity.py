@@ -376,12 +376,17 @@ def test_experts_single_launch_matches_per_expert_oracle(oracle, ccq, cuda, fam,
                                     [1] * 8, [0, 16, 0, 0, 0, 0, 0, 0], [0, 0, 0, 0, 0, 0, 0, 1],
                                     [9, 16, 0, 12, 5, 1, 0, 16]])
 @pytest.mark.parametrize("xdt", ["bf16", "f16"])
-def test_experts_decode_grouped_gemv(oracle, ccq, cuda, counts, xdt):
-    """Decode batches (<= 16 routed rows): one tensor-pipe GEMV launch over the
-    tiles of the experts that have tokens; experts without tokens are skipped."""
+@pytest.mark.parametrize("fam,path", [(2, "rec"), (2, "box"), (0, "box"), (1, "box")])
+def test_experts_decode_grouped_gemv(oracle, ccq, cuda, counts, xdt, fam, path, monkeypatch):
+    """Decode batches (<= 16 routed rows per expert window): one tensor-pipe
+    GEMV launch over the tiles of the experts that have tokens; experts without
+    tokens are skipped.  2.06 on the record kernel and on the TMA-box kernel
+    (CCQ_NO_REC), 2.75 / 2.5 on the TMA-box kernel."""
     torch = cuda
+    if path == "box":
+        monkeypatch.setenv("CCQ_NO_REC", "1")
     E, rows, cols = 8, 48, 1024 + 64
-    secs, offs, x, want = _expert_case(oracle, 2, E, rows, cols, counts, seed=sum(counts) * 3 + 1)
+    secs, offs, x, want = _expert_case(oracle, fam, E, rows, cols, counts, seed=sum(counts) * 3 + 1 + fam)
     ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s_) for s_ in secs])
     tdt = torch.bfloat16 if xdt == "bf16" else torch.float16
     xt = torch.from_numpy(x).to("cuda").to(tdt)
