@@ -438,3 +438,72 @@ def test_experts_shape_errors(oracle, ccq, cuda):
     s1 = oracle.random_packed(64, 192, 2, 64, seed=2)
     with pytest.raises(ccq.ShapeError):
         ccq.Experts.upload([ccq.PackedModel.from_sections(s0), ccq.PackedModel.from_sections(s1)])
+
+
+# ------------------------------------------- BASELINE full sizes (sampled) --
+
+def _slice_rows(oracle, sec, r0, r1):
+    """Rows [r0, r1) of packed sections (the reference's group-major layout)."""
+    g = oracle.group_geometry(sec.family, sec.group_size)
+    gpr = sec.cols // sec.group_size
+    pb = g["payload_bytes"]
+    code = sec.code_payload[r0 * gpr * pb: r1 * gpr * pb].copy()
+    if g["embedded_scale"]:
+        scale = np.zeros(0, np.uint8)
+    else:
+        nib = np.array([(sec.scale_payload[i // 2] >> (4 * (i % 2))) & 0xF
+                        for i in range(r0 * gpr, r1 * gpr)], np.uint16)
+        scale = np.frombuffer(oracle.pack_cluster_scales(nib), np.uint8).copy()
+    cs = sec.cluster_scales[r0:r1] if sec.cluster_scales.size else sec.cluster_scales
+    czp = sec.cluster_zero_points[r0:r1] if sec.cluster_zero_points.size else sec.cluster_zero_points
+    return oracle.Sections(r1 - r0, sec.cols, sec.family, sec.group_size, code, scale,
+                           sec.super_scales[r0:r1].copy(), cs.copy(), czp.copy())
+
+
+@pytest.mark.parametrize("fam", [2, 0, 1])
+def test_prefill_config4_full_size_sampled(oracle, ccq, cuda, fam):
+    """BASELINE configs[4] at full size (8192 -> 28672, M = 4096 tokens) on the
+    tcgen05 GEMM: a 64-row sample of the output checked against the oracle
+    on ALL tokens (2 x 64 x 8192 x 4096 flop on the CPU), plus linearity of
+    the whole product in x."""
+    torch = cuda
+    s = oracle.random_packed(28672, 8192, fam, 64, seed=8192 * 31 + 28672 + fam)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = bf16_round(oracle.random_matrix(4096, 8192, "gaussian", 4097))
+    xt = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+    y = ccq.matmul(d, xt)
+    torch.cuda.synchronize()
+    rows = [(0, 32), (17000, 17032)]
+    for r0, r1 in rows:
+        want = oracle.gemv_batch(_slice_rows(oracle, s, r0, r1), x, threads=8)
+        assert rel_err(y[:, r0:r1].cpu().numpy(), want) < REL_TOL
+    # linearity: W(x1 + x2) == W x1 + W x2 (f32 accumulation tolerance)
+    x2 = torch.from_numpy(bf16_round(oracle.random_matrix(4096, 8192, "gaussian", 4098))).to("cuda").to(torch.bfloat16)
+    xs = (xt.float() + x2.float()).to(torch.bfloat16)
+    lhs = ccq.matmul(d, xs)
+    rhs = y + ccq.matmul(d, x2)
+    exact = (xt.float() + x2.float() - xs.float()).abs().max().item() == 0.0
+    tol = REL_TOL if exact else 1e-2  # bf16 rounding of the sum when not exact
+    assert rel_err(lhs.cpu().numpy(), rhs.cpu().numpy()) < tol
+
+
+@pytest.mark.parametrize("name,E,din,dout,B", [("ERNIE", 64, 8192, 3584, 1), ("ERNIE", 64, 8192, 3584, 64),
+                                               ("DeepSeek", 256, 7168, 2048, 1), ("DeepSeek", 256, 7168, 2048, 16)])
+def test_moe_configs_full_size_sampled(oracle, ccq, cuda, name, E, din, dout, B):
+    """BASELINE configs[2]/[3] at full expert count and shape, top-8 routing:
+    every routed expert's output rows checked against the oracle for the
+    experts on a sample (all for B=1)."""
+    torch = cuda
+    rng = np.random.default_rng(B + E)
+    counts = np.zeros(E, np.int64)
+    for _ in range(B):
+        counts[rng.choice(E, 8, replace=False)] += 1
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    secs = [oracle.random_packed(dout, din, 2, 64, seed=e + 7) for e in range(E)]
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(t) for t in secs])
+    x = bf16_round(oracle.random_matrix(int(offs[-1]), din, "gaussian", 11))
+    y = ccq.experts_matmul(ex, offs, torch.from_numpy(x).to("cuda").to(torch.bfloat16)).cpu().numpy()
+    hit = [e for e in range(E) if counts[e]]
+    for e in hit[:8]:
+        want = oracle.gemv_batch(secs[e], x[offs[e]:offs[e + 1]], threads=8)
+        assert rel_err(y[offs[e]:offs[e + 1]], want) < REL_TOL, (name, e)
