@@ -507,3 +507,29 @@ def test_moe_configs_full_size_sampled(oracle, ccq, cuda, name, E, din, dout, B)
     for e in hit[:8]:
         want = oracle.gemv_batch(secs[e], x[offs[e]:offs[e + 1]], threads=8)
         assert rel_err(y[offs[e]:offs[e + 1]], want) < REL_TOL, (name, e)
+
+
+# ----------------------------------------------------------- randomized sweep --
+
+@pytest.mark.parametrize("seed", list(range(64)))
+def test_randomized_shapes_all_paths(oracle, ccq, cuda, seed):
+    """Seeded random (family, rows, cols, M, dtypes, kernel) cases through the
+    public dispatcher and the forced paths, each against the oracle."""
+    torch = cuda
+    rng = np.random.default_rng(1000 + seed)
+    fam = int(rng.integers(0, 3))
+    rows = int(rng.integers(1, 700))
+    cols = 64 * int(rng.integers(1, 80))
+    M = int(rng.choice([1, 2, 3, 5, 8, 9, 16, 17, 40, 100, 300]))
+    kern = str(rng.choice(["auto", "gemv", "gemm"]))
+    xdt = [torch.bfloat16, torch.float16, torch.float32][int(rng.integers(0, 3))]
+    ydt = [torch.float32, torch.bfloat16][int(rng.integers(0, 2))]
+    s = oracle.random_packed(rows, cols, fam, 64, seed=seed * 7 + 3)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = oracle.random_matrix(M, cols, "gaussian", seed)
+    xt = torch.from_numpy(x).to("cuda").to(xdt)
+    y = ccq.matmul(d, xt, kernel=kern, out_dtype=ydt)
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, xt.float().cpu().numpy(), threads=8)
+    tol = REL_TOL if ydt == torch.float32 else 5e-3
+    assert rel_err(y.float().cpu().numpy(), want) < tol, (fam, rows, cols, M, kern, xdt, ydt)
