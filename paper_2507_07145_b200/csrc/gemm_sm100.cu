@@ -433,10 +433,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
   static_assert(SA == SB, "single ring");
-  uint64_t* full = bars;                        // [SA], 128 decoders + 1 TMA arrival (+tx)
+  uint64_t* full = bars;                        // [SA], 4 decode warps + 1 TMA arrival (+tx)
   uint64_t* empty = full + SA;                  // [SA], mma commit
   uint64_t* code_full = empty + SA;             // [kStagesC], tx
-  uint64_t* code_empty = code_full + kStagesC;  // [kStagesC], count 32 * kDecWarps
+  uint64_t* code_empty = code_full + kStagesC;  // [kStagesC], one arrival per decode warp
   uint64_t* tmem_full = code_empty + kStagesC;  // 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
@@ -469,12 +469,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], 129);
+      mbar_init(&full[s], 5);  // 4 decode warps (one elected lane each) + 1 TMA arrival
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kStagesC; ++s) {
       mbar_init(&code_full[s], 1);
-      mbar_init(&code_empty[s], 32 * kDecWarps);
+      mbar_init(&code_empty[s], kDecWarps);  // one elected lane per decode warp
     }
     mbar_init(tmem_full, 1);
     fence_mbar_init();
@@ -589,7 +589,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (; next_rel < cb_end; ++next_rel) {
         const int rs = next_rel % kStagesC;
         mbar_wait(&code_full[rs], (next_rel / kStagesC) & 1);
-        mbar_arrive(&code_empty[rs]);
+        // one arrival per warp, not per thread: 384 serialized shared-memory
+        // atomics per code block become 12
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&code_empty[rs]);
       }
     };
     for (int st = parity; st < nst; st += kPar) {
@@ -644,7 +647,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&full[s]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
       GT(t_st);
     }
     release_until((nkb + 7) >> 3);
