@@ -740,7 +740,18 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
   const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
   const int64_t xrows = M * xs;  // activation rows (TMA zero-fills past the end)
   void* x16 = nullptr;
-  CCQ_CUDA_TRY(cudaMallocAsync(&x16, size_t(xrows * K) * 2 + size_t(M) * 4 + 16, s));
+  // scratch: the library pool outside graph capture (no re-mapping after
+  // syncs); graph-owned memory (cudaMallocAsync) while capturing
+  int pdev = 0;
+  cudaGetDevice(&pdev);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  cudaMemPool_t pool = scratch_pool(pdev);
+  auto salloc = [&](void** p, size_t bytes) {
+    return capturing ? cudaMallocAsync(p, bytes, s) : cudaMallocFromPoolAsync(p, bytes, pool, s);
+  };
+  CCQ_CUDA_TRY(salloc(&x16, size_t(xrows * K) * 2 + size_t(M) * 4 + 16));
   float* inv_scale = reinterpret_cast<float*>(static_cast<uint8_t*>(x16) + size_t(xrows * K) * 2);
   if (M > 0) {
     const unsigned blocks = unsigned(M);
@@ -795,7 +806,7 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
         const int cb_per = (cblocks + splits - 1) / splits;
         a.kbs = cb_per * 8;
         splits = (cblocks + cb_per - 1) / cb_per;
-        CCQ_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(splits) * size_t(M) * size_t(m->rows) * 4, s));
+        CCQ_CUDA_TRY(salloc(reinterpret_cast<void**>(&part), size_t(splits) * size_t(M) * size_t(m->rows) * 4));
         a.partial = part;
         grid.z = unsigned(splits);
       } else {

@@ -1,3 +1,4 @@
+#include <mutex>
 // Packed-weight upload, per-row widening plans and the synchronous
 // host-buffer entry points of the C ABI (include/ccq_cuda.h).
 //
@@ -119,6 +120,32 @@ bool build_widen_plan(float alpha, float beta, WidenPlan* out, bool invalid[256]
 size_t align_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
 
 }  // namespace
+
+}  // namespace ccqb
+
+namespace ccqb {
+
+cudaMemPool_t scratch_pool(int device) {
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
+  if (device < 0 || device >= 64) device = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaDeviceGetDefaultMemPool(&pool, device);  // fall back to the default pool
+    } else {
+      uint64_t threshold = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    pools[device] = pool;
+  }
+  return pools[device];
+}
 
 }  // namespace ccqb
 
@@ -394,12 +421,20 @@ struct DeviceScope {
   ~DeviceScope() { cudaSetDevice(prev); }
 };
 
+// Scratch for the synchronous host entry points: stream-ordered allocations
+// from the library pool on the legacy stream (no cudaMalloc per call).
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, nullptr);
   }
 };
+
+cudaError_t scratch_alloc(void** p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return cudaMallocFromPoolAsync(p, bytes, ccqb::scratch_pool(dev), nullptr);
+}
 
 }  // namespace
 
@@ -409,7 +444,7 @@ int ccq_dequantize_host(const ccq_dev_model* m, float* out) {
   if (n == 0) return CCQ_OK;
   DeviceScope ds(m->device);
   DevBuf w;
-  CCQ_CUDA_TRY(cudaMalloc(&w.p, n * 4));
+  CCQ_CUDA_TRY(scratch_alloc(&w.p, n * 4));
   int st = launch_decode(m, nullptr, static_cast<float*>(w.p), nullptr);
   if (st != CCQ_OK) return st;
   CCQ_CUDA_TRY(cudaMemcpy(out, w.p, n * 4, cudaMemcpyDeviceToHost));
@@ -429,8 +464,8 @@ int ccq_gemv_batch_host(const ccq_dev_model* m, const float* x, int64_t x_rows, 
   }
   DeviceScope ds(m->device);
   DevBuf dx, dy;
-  CCQ_CUDA_TRY(cudaMalloc(&dx.p, size_t(x_rows * x_cols) * 4));
-  CCQ_CUDA_TRY(cudaMalloc(&dy.p, size_t(y_rows * y_cols) * 4));
+  CCQ_CUDA_TRY(scratch_alloc(&dx.p, size_t(x_rows * x_cols) * 4));
+  CCQ_CUDA_TRY(scratch_alloc(&dy.p, size_t(y_rows * y_cols) * 4));
   CCQ_CUDA_TRY(cudaMemcpy(dx.p, x, size_t(x_rows * x_cols) * 4, cudaMemcpyHostToDevice));
   int st = ccq_cuda_matmul(m, dx.p, CCQ_DTYPE_F32, x_rows, dy.p, CCQ_DTYPE_F32, nullptr);
   if (st != CCQ_OK) return st;
