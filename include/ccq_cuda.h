@@ -167,6 +167,18 @@ int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t* offsets_d
                             const int32_t* offsets_host, const void* x, int x_dtype, void* y,
                             int y_dtype, void* stream);
 
+/* MoE layer with routing: tokens x[T x cols] in natural
+ * order, router top-k expert ids topk_ids[T x k] (device int32) and weights
+ * topk_w[T x k] (device f32) -> y[T x rows_per_expert] =
+ * sum_j topk_w[t,j] * (expert topk_ids[t,j]) x[t], summed in j order.
+ * Permutes the routed rows expert-major, runs ccq_cuda_experts_matmul, and
+ * combines.  Synchronises `stream` once (the grouped launch is sized from the
+ * routing counts); not graph-capturable.  Expert ids outside [0, E) ->
+ * CCQ_ERR_SHAPE. */
+int ccq_cuda_moe_forward(const ccq_dev_model* stack, const int32_t* topk_ids, const float* topk_w,
+                         int64_t T, int32_t k, const void* x, int x_dtype, void* y, int y_dtype,
+                         void* stream);
+
 /* ---- synchronous host-buffer entry points (the reference signatures) ---- */
 
 /* ccq::dequantize (kernels.hpp:36). out: host rows x cols f32. */

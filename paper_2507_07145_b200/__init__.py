@@ -33,7 +33,7 @@ __all__ = [
     "CudaError", "FAMILIES", "PackedModel", "DeviceModel", "load_model", "dequantize", "gemv",
     "gemv_batch", "model_payload_bytes", "group_geometry", "clustered_code_value", "decode",
     "matmul", "grouped", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
-]
+, "moe_forward"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libccq_b200.so")
@@ -101,7 +101,7 @@ ABI_SYMBOLS = [
     "ccq_cuda_gemv", "ccq_cuda_gemm", "ccq_cuda_grouped", "ccq_dequantize_host",
     "ccq_gemv_host", "ccq_gemv_batch_host", "ccq_model_payload_bytes", "ccq_group_geometry",
     "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
-    "ccq_cuda_experts_matmul",
+    "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward",
 ]
 
 _lib = None
@@ -134,6 +134,7 @@ def lib():
         L.ccq_cuda_grouped.argtypes = [vp, i32, vp, vp, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_cuda_experts_upload.argtypes = [vp, i32, C.c_int, C.POINTER(vp)]
         L.ccq_cuda_experts_matmul.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, vp]
+        L.ccq_cuda_moe_forward.argtypes = [vp, vp, vp, i64, i32, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_dequantize_host.argtypes = [vp, vp]
         L.ccq_gemv_host.argtypes = [vp, vp, u64, vp, u64]
         L.ccq_gemv_batch_host.argtypes = [vp, vp, i64, i64, vp, i64, i64]
@@ -418,6 +419,26 @@ def experts_matmul(experts: "Experts", offsets, x, out=None, out_dtype=None, str
     _check(lib().ccq_cuda_experts_matmul(experts.h, offs_dev.data_ptr(), _np_ptr(offs), x.data_ptr(),
                                          _torch_dtype_code(x), out.data_ptr(), _torch_dtype_code(out),
                                          _stream_ptr(stream)))
+    return out
+
+
+def moe_forward(experts: "Experts", topk_ids, topk_weights, x, out=None, out_dtype=None, stream=None):
+    """MoE layer with routing (ccq_cuda_moe_forward): x[T, cols] in token order,
+    topk_ids / topk_weights [T, k] on the device -> y[T, rows_per_expert] =
+    sum_j w[t, j] * expert_{ids[t, j]}(x[t])."""
+    import torch
+    if topk_ids.dtype != torch.int32 or topk_weights.dtype != torch.float32:
+        raise ShapeError("topk_ids must be int32 and topk_weights float32")
+    if topk_ids.shape != topk_weights.shape or topk_ids.dim() != 2 or topk_ids.shape[0] != x.shape[0]:
+        raise ShapeError("topk_ids / topk_weights must be [T, k] with T = x.shape[0]")
+    if not (x.is_contiguous() and topk_ids.is_contiguous() and topk_weights.is_contiguous()):
+        raise ShapeError("operands must be contiguous")
+    if out is None:
+        out = torch.empty(x.shape[0], experts.rows_per_expert, dtype=out_dtype or torch.float32,
+                          device=x.device)
+    _check(lib().ccq_cuda_moe_forward(experts.h, topk_ids.data_ptr(), topk_weights.data_ptr(), x.shape[0],
+                                      topk_ids.shape[1], x.data_ptr(), _torch_dtype_code(x), out.data_ptr(),
+                                      _torch_dtype_code(out), _stream_ptr(stream)))
     return out
 
 

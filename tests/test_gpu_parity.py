@@ -533,3 +533,41 @@ def test_randomized_shapes_all_paths(oracle, ccq, cuda, seed):
     want = oracle.gemv_batch(s, xt.float().cpu().numpy(), threads=8)
     tol = REL_TOL if ydt == torch.float32 else 5e-3
     assert rel_err(y.float().cpu().numpy(), want) < tol, (fam, rows, cols, M, kern, xdt, ydt)
+
+
+# ------------------------------------------------ MoE routing (permute/combine) --
+
+@pytest.mark.parametrize("fam", [2, 0, 1])
+@pytest.mark.parametrize("T,k,E", [(1, 8, 16), (5, 2, 6), (40, 8, 16), (300, 4, 8)])
+def test_moe_forward_routing(oracle, ccq, cuda, fam, T, k, E):
+    """Token-order x + router top-k -> weighted sum of the experts' outputs,
+    against the oracle composition y[t] = sum_j w[t,j] * gemv(expert e(t,j), x[t])."""
+    torch = cuda
+    rows, cols = 48, 512
+    rng = np.random.default_rng(T * 31 + k + fam)
+    ids = np.stack([rng.choice(E, k, replace=False) for _ in range(T)]).astype(np.int32)
+    w = rng.random((T, k)).astype(np.float32)
+    secs = [oracle.random_packed(rows, cols, fam, 64, seed=e + 50 * fam) for e in range(E)]
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(t) for t in secs])
+    x = bf16_round(oracle.random_matrix(T, cols, "gaussian", T))
+    y = ccq.moe_forward(ex, torch.from_numpy(ids).cuda(), torch.from_numpy(w).cuda(),
+                        torch.from_numpy(x).cuda().to(torch.bfloat16))
+    torch.cuda.synchronize()
+    want = np.zeros((T, rows), np.float64)
+    for e in range(E):
+        tok, slot = np.nonzero(ids == e)
+        if tok.size:
+            ye = oracle.gemv_batch(secs[e], x[tok], threads=8)
+            for i in range(tok.size):
+                want[tok[i]] += float(w[tok[i], slot[i]]) * ye[i]
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
+
+
+def test_moe_forward_rejects_bad_expert_ids(ccq, cuda):
+    torch = cuda
+    from paper_2507_07145_b200.synthetic import random_packed
+    ex = ccq.Experts.upload([random_packed(32, 256, 2, 64, e) for e in range(4)])
+    ids = torch.tensor([[0, 7]], dtype=torch.int32, device="cuda")
+    w = torch.ones(1, 2, device="cuda")
+    with pytest.raises(ccq.ShapeError):
+        ccq.moe_forward(ex, ids, w, torch.randn(1, 256, device="cuda").to(torch.bfloat16))
