@@ -33,7 +33,8 @@ __all__ = [
     "CudaError", "FAMILIES", "PackedModel", "DeviceModel", "load_model", "dequantize", "gemv",
     "gemv_batch", "model_payload_bytes", "group_geometry", "clustered_code_value", "decode",
     "matmul", "grouped", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
-, "moe_forward"]
+    "moe_forward",
+]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libccq_b200.so")
