@@ -124,6 +124,10 @@ __device__ __forceinline__ void load4(const void* x, int64_t base, float (&v)[4]
 template <int FAM, int XDT, int XS>
 __global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __half* __restrict__ out,
                                                  float* __restrict__ inv_scale, int64_t K) {
+  // PDL: the GEMM behind this kernel may start its weight loads and decode
+  // now; x belongs to the previous kernel until the wait returns.
+  griddep_launch_dependents();
+  griddep_wait();
   const int64_t m = blockIdx.x;
   const int64_t nq = K / 4;
   float mx = 0.f;
@@ -202,6 +206,8 @@ __global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __h
 #ifdef CCQ_GEMM_TRACE
 }  // namespace
 __device__ unsigned long long g_gtrace[4096 * 8];
+__device__ unsigned long long g_gtrace2[4096 * 4];  // per decode warp: first code wait, long waits, max wait; producer
+__device__ int g_gexp;  // experiment: 1 skip decode math, 2 skip MMAs, 3 skip TMEM stores
 namespace {
 __device__ __forceinline__ unsigned long long gclk() {
   unsigned long long t;
@@ -430,7 +436,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kStagesC = SM::SC;
   constexpr int kCodeBox = GF<FAM>::BOXB;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-align by offset (not through an integer cast, which would turn
+  // every smem access of the decoders into a generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::OFF_BAR);
   static_assert(SA == SB, "single ring");
   uint64_t* full = bars;                        // [SA], 4 decode warps + 1 TMA arrival (+tx)
@@ -441,6 +449,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // PDL: the launch behind this one (split-K reduce, the next layer's
+  // prepass) waits for this grid's completion itself, so it may be scheduled now.
+  griddep_launch_dependents();
+  // Weights (codes, nibbles, plans, super scales) are static; the activation
+  // tile, inv_scale, y and the routing offsets belong to the previous kernel
+  // until griddepcontrol.wait: the B producer and the epilogue wait, and in
+  // grouped mode every thread waits before reading the offsets.
+  if (a.offsets) griddep_wait();
   // Tile: weight rows [r0, row_end), tokens [n0, tok_end); y row stride y_ld,
   // y column of row r is r - y_col0.
   // The tile covers BN activation rows = BN / xs tokens.
@@ -495,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpB) {
     if (lane == 0) {
       // ---------------- TMA producer: activation tiles ----------------
+      griddep_wait();
       for (int st = 0; st < nst; ++st) {
         const int s = st % SB;
         const int ng = nkb - st * G < G ? nkb - st * G : G;
@@ -508,15 +525,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kWarpCodes) {
     if (lane == 0) {
       // ---------------- TMA producer: packed codes (runs ahead on its own ring) ----
+#ifdef CCQ_GEMM_TRACE
+      unsigned long long pw = 0;
+#endif
       for (int cb = 0; cb * 8 < nkb; ++cb) {
         const int kb = kb0 + cb * 8, cs = cb % kStagesC;
+#ifdef CCQ_GEMM_TRACE
+        const unsigned long long tp = gclk();
+#endif
         mbar_wait(&code_empty[cs], ((cb / kStagesC) + 1) & 1);
+#ifdef CCQ_GEMM_TRACE
+        pw += gclk() - tp;
+#endif
         mbar_arrive_expect_tx(&code_full[cs], SM::C_BYTES + SM::N_BYTES);
         const int c = kb / kChunk, jb = (kb % kChunk) / 8;
         const int y = int(int64_t(c) * a.rows_pad + r0);
         tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES, &tm_codes, jb * kCodeBox, y, &code_full[cs]);
         if constexpr (GF<FAM>::NIB) tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
       }
+#ifdef CCQ_GEMM_TRACE
+      if (blockIdx.x == 0 && blockIdx.y < 320) g_gtrace2[(blockIdx.y * kDecWarps) * 4 + 3] = pw;
+#endif
     }
   } else if (warp == kWarpMma) {
     if (lane == 0) {
@@ -537,6 +566,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         tc_fence_after();
         const uint32_t b_base = smem_addr(smem + SM::OFF_B + s * SM::B_BYTES);
+#ifdef CCQ_GEMM_TRACE
+        const unsigned long long tb0 = gclk();
+        if (g_gexp != 2)
+#endif
         for (int gg = 0; gg < ng; ++gg) {
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
@@ -549,6 +582,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                          (st | gg | k) != 0);
           }
         }
+#ifdef CCQ_GEMM_TRACE
+        wb += gclk() - tb0;
+#endif
         mma_commit(&empty[s]);
       }
       mma_commit(tmem_full);
@@ -566,9 +602,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = quad * 32 + lane;         // tile row == TMEM lane
     const int64_t row = r0 + r;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
+    // Rows past row_end decode row_end-1's plan (their output is never
+    // stored); an unconditional load keeps M a known 32-bit operand, so
+    // the widening stays one IMAD.HI (a select here costs 2 more IMADs/byte).
     WidenPlan pl = WidenPlan{0, 0, plan_sel(0)};
-    if constexpr (FAM == kF206)
-      if (row < row_end) pl = a.plan[row];
+    if constexpr (FAM == kF206) pl = a.plan[row < row_end ? row : row_end - 1];
     const uint32_t selb = pl.sel & 0xFFFFu, step = pl.sel >> 16;
     const uint32_t sel[4] = {selb, selb + step, selb + 2 * step, selb + 3 * step};
     uint32_t magic, mask, shift26;
@@ -577,6 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("mov.b32 %0, 0x04000000;" : "=r"(shift26));
 #ifdef CCQ_GEMM_TRACE
     unsigned long long t_code = 0, t_dec = 0, t_empty = 0, t_st = 0, t_prev = gclk(), t0 = t_prev;
+    unsigned long long x_first = 0, x_long = 0, x_max = 0;
 #define GT(var) { const unsigned long long _t = gclk(); var += _t - t_prev; t_prev = _t; }
 #else
 #define GT(var)
@@ -603,10 +642,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cb = kb >> 3, cs = cb % kStagesC, j = kb & 7;
       release_until(cb);
       const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
+#ifdef CCQ_GEMM_TRACE
+      const unsigned long long tcw = gclk();
+#endif
       mbar_wait(&code_full[cs], (cb / kStagesC) & 1);
+#ifdef CCQ_GEMM_TRACE
+      {
+        const unsigned long long d = gclk() - tcw;
+        if (kb == 0) x_first = gclk() - t0;
+        if (d > 1000) ++x_long;
+        if (d > x_max) x_max = d;
+      }
+#endif
       GT(t_code);
       uint32_t h[32];
       uint32_t h2[SPLIT == 2 ? 32 : 1];
+#ifdef CCQ_GEMM_TRACE
+      if (g_gexp == 1) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) h[i] = magic + i;
+        if constexpr (SPLIT == 2)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) h2[i] = magic + i;
+      } else
+#endif
       if constexpr (FAM == kF206) {
         const int jb = ((kb0 + kb) % kChunk) / 8;
         uint32_t nibword;
@@ -627,7 +686,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t qb = prmt(words[byte >> 2], 0u, sel[byte & 3]);
           const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);  // code at [8,23)
           const uint32_t w2 = prmt(hi, 0u, 0x2121u);                        // code | code << 16
-          const uint32_t w3 = __umulhi(w2, shift26);                         // w2 >> 6
+#ifndef CCQ_GEMM_W3
+#define CCQ_GEMM_W3 2
+#endif
+          // w2 >> 6 on the ALU (SHF) or the FMA pipe (IMAD.HI); mixed to balance the two
+          const uint32_t w3 = CCQ_GEMM_W3 == 2 || (CCQ_GEMM_W3 == 1 && (byte & 1)) ? (w2 >> 6) : __umulhi(w2, shift26);
           h[2 * byte] = hfma2_u32(lop_mask_or(w2, mask, magic), scu, biasu);     // (s3, 8 s2)
           h[2 * byte + 1] = hfma2_u32(lop_mask_or(w3, mask, magic), scu, biasu); // (s1, 8 s0)
         }
@@ -642,8 +705,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         GT(t_empty);
         tc_fence_after();
       }
+#ifdef CCQ_GEMM_TRACE
+      if (g_gexp == 3) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc ^= h[i];
+        if (acc == 0x12345678u) g_gtrace[4095 * 8] = acc;  // keep the decode alive
+      } else {
+#endif
       tmem_st32(tmem_a + lane_base + ((s * G + gg) * SPLIT) * kACols, h);
       if constexpr (SPLIT == 2) tmem_st32(tmem_a + lane_base + ((s * G + gg) * SPLIT + 1) * kACols, h2);
+#ifdef CCQ_GEMM_TRACE
+      }
+#endif
       }
       tmem_st_wait();
       tc_fence_before();
@@ -657,12 +731,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int slot = (blockIdx.y * kDecWarps + warp) * 8;
       g_gtrace[slot + 0] = t_code; g_gtrace[slot + 1] = t_dec; g_gtrace[slot + 2] = t_empty;
       g_gtrace[slot + 3] = t_st; g_gtrace[slot + 4] = gclk() - t0;
+      const int s2 = (blockIdx.y * kDecWarps + warp) * 4;
+      g_gtrace2[s2 + 0] = x_first; g_gtrace2[s2 + 1] = x_long; g_gtrace2[s2 + 2] = x_max;
     }
 #endif
 
     // ---------------- epilogue: 32-column slices round-robin over the groups ----
     mbar_wait(tmem_full, 0);
     tc_fence_after();
+    griddep_wait();  // inv_scale and y (long complete by now)
     const float sup = row < row_end ? a.super[row] : 0.f;
 #pragma unroll 1
     for (int cc = parity * 32; cc < BN; cc += 32 * kPar) {
@@ -718,6 +795,7 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ p
                                                      int64_t rows, const float* __restrict__ super,
                                                      const float* __restrict__ inv_scale, void* y, int y_dtype) {
   const int64_t total = M * rows;
+  griddep_wait();  // the partial sums are the GEMM's
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     float v = 0.f;
     for (int z = 0; z < splits; ++z) v += part[size_t(z) * size_t(total) + size_t(i)];
@@ -755,13 +833,19 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
   float* inv_scale = reinterpret_cast<float*>(static_cast<uint8_t*>(x16) + size_t(xrows * K) * 2);
   if (M > 0) {
     const unsigned blocks = unsigned(M);
+    __half* xh = static_cast<__half*>(x16);
+    cudaError_t pe;
     if (x_dtype == CCQ_DTYPE_F32)
-      x_prepass<FAM, CCQ_DTYPE_F32, 2><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
+      pe = launch_pdl(x_prepass<FAM, CCQ_DTYPE_F32, 2>, dim3(blocks), dim3(256), 0, s, x, xh, inv_scale, K);
     else if (x_dtype == CCQ_DTYPE_BF16)
-      x_prepass<FAM, CCQ_DTYPE_BF16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
+      pe = launch_pdl(x_prepass<FAM, CCQ_DTYPE_BF16, 1>, dim3(blocks), dim3(256), 0, s, x, xh, inv_scale, K);
     else
-      x_prepass<FAM, CCQ_DTYPE_F16, 1><<<blocks, 256, 0, s>>>(x, static_cast<__half*>(x16), inv_scale, K);
+      pe = launch_pdl(x_prepass<FAM, CCQ_DTYPE_F16, 1>, dim3(blocks), dim3(256), 0, s, x, xh, inv_scale, K);
     count_launch();
+    if (pe != cudaSuccess) {
+      cudaFreeAsync(x16, s);
+      return cuda_fail(pe, "gemm prepass launch");
+    }
   }
   CUtensorMap tm_codes, tm_nib, tm_x;
   int st = make_map_2d(&tm_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, m->codes, m->rec,
@@ -815,13 +899,19 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
     }
   }
   if (grid.x && grid.y) {
-    kern<<<grid, kThreads, SM::TOTAL, s>>>(tm_codes, tm_nib, tm_x, a);
+    cudaError_t le = launch_pdl(kern, grid, dim3(kThreads), SM::TOTAL, s, tm_codes, tm_nib, tm_x, a);
     count_launch();
-    if (part) {
+    if (le == cudaSuccess && part) {
       const int64_t total = M * m->rows;
       const unsigned blocks = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 8));
-      splitk_reduce<<<blocks, 256, 0, s>>>(part, splits, M, m->rows, m->super, inv_scale, y, y_dtype);
+      le = launch_pdl(splitk_reduce, dim3(blocks), dim3(256), 0, s, static_cast<const float*>(part), splits, M,
+                      m->rows, m->super, static_cast<const float*>(inv_scale), y, y_dtype);
       count_launch();
+    }
+    if (le != cudaSuccess) {
+      if (part) cudaFreeAsync(part, s);
+      cudaFreeAsync(x16, s);
+      return cuda_fail(le, "gemm launch");
     }
   }
   cudaError_t e = cudaGetLastError();
@@ -882,6 +972,11 @@ int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const
 }  // namespace ccqb
 
 #ifdef CCQ_GEMM_TRACE
+extern "C" int ccq_gemm_trace_dump2(unsigned long long* host, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, ccqb::g_gtrace2, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+extern "C" int ccq_gemm_trace_exp(int e) { return cudaMemcpyToSymbol(ccqb::g_gexp, &e, sizeof(int)) == cudaSuccess ? 0 : 1; }
 extern "C" int ccq_gemm_trace_dump(unsigned long long* host, int n) {
   cudaDeviceSynchronize();
   return cudaMemcpyFromSymbol(host, ccqb::g_gtrace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
