@@ -548,12 +548,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     }
   } else if (warp == kWarpMma) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer (whole warp, converged; one elected lane issues) ----
+    {
       constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
 #ifdef CCQ_GEMM_TRACE
       unsigned long long wa = 0, wb = 0, t0m = gclk();
 #endif
+      // B descriptors: one base per stage, + (byte offset >> 4) per group / K step
+      const uint64_t db_ring = smem_desc(smem_addr(smem + SM::OFF_B), 16, 1024, 2);
       for (int st = 0; st < nst; ++st) {
         const int s = st % SA;
         const int ng = nkb - st * G < G ? nkb - st * G : G;
@@ -565,31 +567,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], (st / SA) & 1);
 #endif
         tc_fence_after();
-        const uint32_t b_base = smem_addr(smem + SM::OFF_B + s * SM::B_BYTES);
+        const uint64_t db_s = db_ring + uint64_t((s * SM::B_BYTES) >> 4);
+        const uint32_t ta_s = tmem_a + (s * G * SPLIT) * kACols;
 #ifdef CCQ_GEMM_TRACE
         const unsigned long long tb0 = gclk();
         if (g_gexp != 2)
 #endif
-        for (int gg = 0; gg < ng; ++gg) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // A from TMEM (lane = weight row, 8 columns per K = 16);
-            // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
-            const uint64_t db = smem_desc(b_base + gg * SM::B_BLOCK + k * 32, 16, 1024, 2);
+        for (int gg = 0; gg < G; ++gg) {
+          if (gg < ng) {
 #pragma unroll
-            for (int h = 0; h < SPLIT; ++h)
-              mma_f16_ts(tmem_d + h * BN, tmem_a + ((s * G + gg) * SPLIT + h) * kACols + k * 8, db, idesc,
-                         (st | gg | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              // A from TMEM (lane = weight row, 8 columns per K = 16);
+              // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
+              const uint64_t db = db_s + uint64_t((gg * SM::B_BLOCK + k * 32) >> 4);
+#pragma unroll
+              for (int h = 0; h < SPLIT; ++h)
+                mma_f16_ts_warp(tmem_d + h * BN, ta_s + (gg * SPLIT + h) * kACols + k * 8, db, idesc,
+                                (st | gg | k) != 0);
+            }
           }
         }
 #ifdef CCQ_GEMM_TRACE
         wb += gclk() - tb0;
 #endif
-        mma_commit(&empty[s]);
+        mma_commit_warp(&empty[s]);
       }
-      mma_commit(tmem_full);
+      mma_commit_warp(tmem_full);
 #ifdef CCQ_GEMM_TRACE
-      if (blockIdx.x == 0 && blockIdx.y < 320) {
+      if (lane == 0 && blockIdx.x == 0 && blockIdx.y < 320) {
         const int slot = (blockIdx.y * kDecWarps) * 8;
         g_gtrace[slot + 5] = wa; g_gtrace[slot + 6] = wb; g_gtrace[slot + 7] = gclk() - t0m;
       }
@@ -634,14 +640,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&code_empty[rs]);
       }
     };
+    static_assert(8 % G == 0, "a stage must lie inside one 8-group code block");
     for (int st = parity; st < nst; st += kPar) {
+      // per stage: one code block, one code_full wait, one nibble word
       const int s = st % SA;
       const int ng = nkb - st * G < G ? nkb - st * G : G;
-      for (int gg = 0; gg < ng; ++gg) {
-      const int kb = st * G + gg;
-      const int cb = kb >> 3, cs = cb % kStagesC, j = kb & 7;
+      const int kbs = st * G;
+      const int cb = kbs >> 3, cs = cb % kStagesC;
       release_until(cb);
-      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
 #ifdef CCQ_GEMM_TRACE
       const unsigned long long tcw = gclk();
 #endif
@@ -649,12 +655,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef CCQ_GEMM_TRACE
       {
         const unsigned long long d = gclk() - tcw;
-        if (kb == 0) x_first = gclk() - t0;
+        if (kbs == 0) x_first = gclk() - t0;
         if (d > 1000) ++x_long;
         if (d > x_max) x_max = d;
       }
 #endif
       GT(t_code);
+      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
+      uint32_t nibword = 0;
+      if constexpr (FAM == kF206)
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
+                     : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + (((kb0 + kbs) % kChunk) / 8) * 4)));
+      for (int gg = 0; gg < ng; ++gg) {
+      const int j = (kbs & 7) + gg;
       uint32_t h[32];
       uint32_t h2[SPLIT == 2 ? 32 : 1];
 #ifdef CCQ_GEMM_TRACE
@@ -667,10 +680,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else
 #endif
       if constexpr (FAM == kF206) {
-        const int jb = ((kb0 + kb) % kChunk) / 8;
-        uint32_t nibword;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
-                     : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + jb * 4)));
         const uint4 cw = lds128(cstage + r * kCodeBox + ((j ^ (r & 7)) << 4));
         const uint32_t sc = (nibword >> (4 * j)) & 0xFu;
         // half2 (sc, sc) and bias (-(1024+32) sc, -(1024+256) sc), exact in f16
