@@ -9,6 +9,9 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2507_07145_b200 as P  # noqa: E402
 
+if os.environ.get("CCQ_LIB"):  # experiment builds (tools only)
+    P.LIB_PATH = os.path.join(os.path.dirname(P.__file__), os.environ["CCQ_LIB"])
+
 peaks = bench.load_peaks()
 dev = torch.device("cuda", 0)
 s = torch.cuda.Stream()
