@@ -394,14 +394,19 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   int st = check_dtypes(x_dtype, y_dtype);
   if (st != CCQ_OK || M == 0 || m->rows == 0) return st;
   // Dispatch by batch (measured, profiles/r01_sweep.json): M = 1 on the
-  // CUDA-core streaming GEMV; 2 <= M <= 8 (bf16/f16 activations) on the
+  // CUDA-core streaming GEMV; 2 <= M <= 8 (2.06: see below; bf16/f16 activations) on the
   // tensor-pipe GEMV when all tokens fit one launch; the tcgen05 GEMM above
   // that, or when the activations would not fit; f32 activations (the
   // reference's own f32 API) take the streaming GEMV at M = 1 and the GEMM's
   // exact hi/lo split otherwise.
   const bool mma = x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
                    gemv_mma_supported(m, M);
-  if (mma && M >= mma_min_tokens() && (gemv_mma_fits(m, M) || !gemm_supported(m, M)))
+  // 2.06 hands over to the GEMM earlier: at M >= 7, and at M >= 3 on
+  // K-heavy layers (cols > rows, few 16-row tiles but long x staging), the
+  // tcgen05 GEMM is faster (profiles/r01_dispatch_thresholds.txt).
+  const bool gemm_earlier = m->family == kF206 && (M >= 7 || (m->cols > m->rows && M >= 3));
+  if (mma && M >= mma_min_tokens() &&
+      ((gemv_mma_fits(m, M) && !(gemm_earlier && gemm_supported(m, M))) || !gemm_supported(m, M)))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
   if (!gemv_fast_supported(m, M) && gemm_supported(m, M))
     return launch_gemm(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));

@@ -50,7 +50,7 @@ for shp in a.shapes.split(","):
             e1.record(s)
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / (a.reps * copies)
-        print(json.dumps({"family": a.family, "d_in": din, "d_out": dout, "M": M, "us": round(us, 2),
+        print(json.dumps({"family": a.family, "kernel": a.kernel, "d_in": din, "d_out": dout, "M": M, "us": round(us, 2),
                           "packed_GBps": round(pb / us / 1e3, 1), "hbm_frac": round(pb / us / 1e3 / peak_bw, 3),
                           "TFLOPs": round(2 * M * din * dout / us / 1e6, 1)}))
         del g
