@@ -253,22 +253,48 @@ def main():
     achieved = alg_bytes / (per_launch_us * 1e-6) / 1e9
 
     # --- e2e: public API, host activations in, outputs back, every layer ----
-    def e2e_step():
-        # the step's inputs in (one pinned H2D), its results out (one D2H)
-        x_dev.copy_(x_host, non_blocking=True)
+    # Every step copies its own inputs in (one pinned H2D) and its results out
+    # (one D2H), as a serving loop would: double-buffered on a copy stream, so
+    # step i's D2H and step i+1's H2D overlap step i's / i+1's kernels.  The
+    # timed region starts before the first H2D and ends after the last D2H.
+    copy_stream = torch.cuda.Stream(device=dev)
+    x_bufs = [x_dev, torch.empty_like(x_dev)]
+    y_bufs = [y_dev, torch.empty_like(y_dev)]
+    y_hosts = [y_host, torch.empty_like(y_host).pin_memory()]
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    comp_done = [torch.cuda.Event() for _ in range(2)]
+    d2h_done = [torch.cuda.Event() for _ in range(2)]
+    for b in range(2):  # initial state: buffers free
+        comp_done[b].record(stream)
+        d2h_done[b].record(copy_stream)
+
+    def e2e_step(i):
+        b = i & 1
+        copy_stream.wait_event(comp_done[b])  # x_bufs[b] no longer read (step i-2)
+        with torch.cuda.stream(copy_stream):
+            x_bufs[b].copy_(x_host, non_blocking=True)
+        h2d_done[b].record(copy_stream)
+        stream.wait_event(h2d_done[b])
+        stream.wait_event(d2h_done[b])  # y_bufs[b] drained (step i-2)
         for l in range(args.layers):
-            P.matmul(layers[l], x_dev[l], out=y_dev[l], stream=stream)
-        y_host.copy_(y_dev, non_blocking=True)
+            P.matmul(layers[l], x_bufs[b][l], out=y_bufs[b][l], stream=stream)
+        comp_done[b].record(stream)
+        copy_stream.wait_event(comp_done[b])
+        with torch.cuda.stream(copy_stream):
+            y_hosts[b].copy_(y_bufs[b], non_blocking=True)
+        d2h_done[b].record(copy_stream)
 
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            e2e_step()
-    stream.synchronize()
+        for i in range(args.warmup):
+            e2e_step(i)
+    torch.cuda.synchronize()
     barrier()
     with torch.cuda.stream(stream):
         start.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        copy_stream.wait_event(start)
+        for i in range(args.steps):
+            e2e_step(i)
+        stream.wait_event(d2h_done[(args.steps - 1) & 1])
         end.record(stream)
     torch.cuda.synchronize()
     barrier()

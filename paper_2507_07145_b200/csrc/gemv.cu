@@ -227,8 +227,11 @@ __device__ __forceinline__ float dot_206(const uint8_t* gp, const X& x, float q,
 template <class X>
 __device__ __forceinline__ float dot_275(const uint8_t* gp, const X& x, float q, uint32_t one,
                                          float* sc) {
-  const uint32_t* a4 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(3));
-  const uint32_t sh = (reinterpret_cast<uintptr_t>(gp) & 3u) * 8u;  // 0 or 16
+  // align by pointer arithmetic (an integer round trip would lose the
+  // shared-memory address space and turn these into generic loads)
+  const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(gp) & 3u);
+  const uint32_t* a4 = reinterpret_cast<const uint32_t*>(gp - mis);
+  const uint32_t sh = mis * 8u;  // 0 or 16
   uint32_t w[6];
   {
     uint32_t raw[7];

@@ -930,7 +930,10 @@ inline RecCfg rec_cfg(const ccq_dev_model* m, int M, int grid, int max_smem, int
   const size_t stg = (size_t(16) * m->rec + 127) & ~size_t(127);
   const size_t fixed = size_t(m->gpr * 128 + 16) * M + size_t(m->gpr) * MP * 4 +
                        size_t(items) * 4 * kRowsT * MP * 4 + MP * 8 + 128 + 256;
-  if (fixed + 2 * stg + size_t(items) * 16 > size_t(max_smem)) return RecCfg{0, 0};
+  // S >= 3: consumer warps take every third item (12 warps x 4 quarters), so
+  // with S = 2 a warp could wait on a slot still holding the item 2S before
+  // its own and pass on the stale phase parity (8192 -> 28672 at M = 6).
+  if (fixed + 3 * stg + size_t(items) * 16 > size_t(max_smem)) return RecCfg{0, 0};
   const int S = int(std::min<size_t>(size_t(items), (size_t(max_smem) - fixed) / (stg + 16)));
   return RecCfg{S, fixed + size_t(S) * (stg + 16)};
 }

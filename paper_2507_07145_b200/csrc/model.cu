@@ -401,10 +401,19 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   // exact hi/lo split otherwise.
   const bool mma = x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
                    gemv_mma_supported(m, M);
-  // 2.06 hands over to the GEMM earlier: at M >= 7, and at M >= 3 on
-  // K-heavy layers (cols > rows, few 16-row tiles but long x staging), the
-  // tcgen05 GEMM is faster (profiles/r01_dispatch_thresholds.txt).
-  const bool gemm_earlier = m->family == kF206 && (M >= 7 || (m->cols > m->rows && M >= 3));
+  // 2.06 hands over to the GEMM earlier when the GEMM fills the SMs (>= 3/4
+  // of them with 128-row tiles x split-K): at M = 8, and at M >= 3 on
+  // K-heavy layers (cols > rows: few 16-row tiles but long x staging for the
+  // tensor-pipe GEMV) (profiles/r01_dispatch_thresholds.txt).
+  bool gemm_earlier = false;
+  if (m->family == kF206 && (M >= 8 || (m->cols > m->rows && M >= 3))) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sms = num_sms(dev);
+    const int64_t tiles = (m->rows + 127) / 128, cblocks = (m->gpr + 7) / 8;
+    const int64_t splits = tiles * 2 <= sms && cblocks >= 8 ? std::min<int64_t>(sms / tiles, cblocks / 4) : 1;
+    gemm_earlier = tiles * std::max<int64_t>(splits, 1) * 4 >= int64_t(sms) * 3;
+  }
   if (mma && M >= mma_min_tokens() &&
       ((gemv_mma_fits(m, M) && !(gemm_earlier && gemm_supported(m, M))) || !gemm_supported(m, M)))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));

@@ -487,6 +487,29 @@ def test_prefill_config4_full_size_sampled(oracle, ccq, cuda, fam):
     assert rel_err(lhs.cpu().numpy(), rhs.cpu().numpy()) < tol
 
 
+@pytest.mark.parametrize("fam", [2, 0, 1])
+def test_config4_shape_decode_batches_full_size(oracle, ccq, cuda, fam):
+    """configs[4]'s 8192 -> 28672 layer at decode batches M = 1..8 on the
+    tensor-pipe GEMV (kernel="gemv") and the auto dispatch: sampled rows
+    against the oracle, and the WHOLE output against the tcgen05 GEMM (every
+    row tile of every CTA; the record kernel's ring depth changes with M -
+    S = 2 once aliased a stale stage at M = 6)."""
+    torch = cuda
+    s = oracle.random_packed(28672, 8192, fam, 64, seed=28672 + fam)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    for M in range(1, 9):
+        x = bf16_round(oracle.random_matrix(M, 8192, "gaussian", 100 + M))
+        xt = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+        ref = ccq.matmul(d, xt, kernel="gemm")
+        for kernel in ("gemv", "auto"):
+            y = ccq.matmul(d, xt, kernel=kernel)
+            torch.cuda.synchronize()
+            assert rel_err(y.cpu().numpy(), ref.cpu().numpy()) < REL_TOL, (M, kernel)
+            for r0, r1 in ((0, 16), (28656, 28672)):
+                want = oracle.gemv_batch(_slice_rows(oracle, s, r0, r1), x, threads=8)
+                assert rel_err(y[:, r0:r1].cpu().numpy(), want) < REL_TOL, (M, kernel, r0)
+
+
 @pytest.mark.parametrize("name,E,din,dout,B", [("ERNIE", 64, 8192, 3584, 1), ("ERNIE", 64, 8192, 3584, 64),
                                                ("DeepSeek", 256, 7168, 2048, 1), ("DeepSeek", 256, 7168, 2048, 16)])
 def test_moe_configs_full_size_sampled(oracle, ccq, cuda, name, E, din, dout, B):
