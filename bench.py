@@ -254,10 +254,11 @@ def main():
 
     # --- e2e: public API, host activations in, outputs back, every layer ----
     # Every step copies its own inputs in (one pinned H2D) and its results out
-    # (one D2H), as a serving loop would: double-buffered on a copy stream, so
-    # step i's D2H and step i+1's H2D overlap step i's / i+1's kernels.  The
+    # (one D2H), as a serving loop would: double-buffered on two copy streams;
+    # step i+1's H2D and step i's D2H overlap step i's / i+1's kernels.  The
     # timed region starts before the first H2D and ends after the last D2H.
-    copy_stream = torch.cuda.Stream(device=dev)
+    h2d_stream = torch.cuda.Stream(device=dev)  # separate copy streams: an H2D
+    d2h_stream = torch.cuda.Stream(device=dev)  # never queues behind a D2H
     x_bufs = [x_dev, torch.empty_like(x_dev)]
     y_bufs = [y_dev, torch.empty_like(y_dev)]
     y_hosts = [y_host, torch.empty_like(y_host).pin_memory()]
@@ -266,34 +267,43 @@ def main():
     d2h_done = [torch.cuda.Event() for _ in range(2)]
     for b in range(2):  # initial state: buffers free
         comp_done[b].record(stream)
-        d2h_done[b].record(copy_stream)
+        d2h_done[b].record(d2h_stream)
 
-    def e2e_step(i):
+    def issue_h2d(i):
         b = i & 1
-        copy_stream.wait_event(comp_done[b])  # x_bufs[b] no longer read (step i-2)
-        with torch.cuda.stream(copy_stream):
+        h2d_stream.wait_event(comp_done[b])  # x_bufs[b] no longer read (step i-2)
+        with torch.cuda.stream(h2d_stream):
             x_bufs[b].copy_(x_host, non_blocking=True)
-        h2d_done[b].record(copy_stream)
+        h2d_done[b].record(h2d_stream)
+
+    def e2e_step(i, n):
+        # step i's input was copied in while step i-1 ran (step 0: here)
+        b = i & 1
+        if i == 0:
+            issue_h2d(0)
+        if i + 1 < n:
+            issue_h2d(i + 1)
         stream.wait_event(h2d_done[b])
         stream.wait_event(d2h_done[b])  # y_bufs[b] drained (step i-2)
         for l in range(args.layers):
             P.matmul(layers[l], x_bufs[b][l], out=y_bufs[b][l], stream=stream)
         comp_done[b].record(stream)
-        copy_stream.wait_event(comp_done[b])
-        with torch.cuda.stream(copy_stream):
+        d2h_stream.wait_event(comp_done[b])
+        with torch.cuda.stream(d2h_stream):
             y_hosts[b].copy_(y_bufs[b], non_blocking=True)
-        d2h_done[b].record(copy_stream)
+        d2h_done[b].record(d2h_stream)
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            e2e_step(i)
+            e2e_step(i, args.warmup)
     torch.cuda.synchronize()
     barrier()
     with torch.cuda.stream(stream):
         start.record(stream)
-        copy_stream.wait_event(start)
+        h2d_stream.wait_event(start)
+        d2h_stream.wait_event(start)
         for i in range(args.steps):
-            e2e_step(i)
+            e2e_step(i, args.steps)
         stream.wait_event(d2h_done[(args.steps - 1) & 1])
         end.record(stream)
     torch.cuda.synchronize()
