@@ -59,23 +59,30 @@ int geometry_for(int family, int group_size, Geometry* g) {
 
 namespace {
 
-// Reference widening (coding.hpp:144): lround in double.
-inline long ref_widen(int q, float a, float b) {
+// Reference widening (coding.hpp:144): lround(q * alpha + beta) in double,
+// multiply and add rounded separately (no FMA contraction on the device).
+__host__ __device__ inline long ref_widen(int q, float a, float b) {
+#ifdef __CUDA_ARCH__
+  return lround(__dadd_rn(__dmul_rn(double(q), double(a)), double(b)));
+#else
   return std::lround(double(q) * double(a) + double(b));
+#endif
 }
 
-// Builds the exact fixed-point plan of one row and marks the q values the
-// reference would reject (result outside [0, 2^15)).  Returns false if no
-// plan reproduces the reference for every valid q.
-bool build_widen_plan(float alpha, float beta, WidenPlan* out, bool invalid[256]) {
-  long ref[256];
+// Builds the exact fixed-point plan of one row and marks (bit q of inv[8]) the
+// q values the reference would reject (result outside [0, 2^15)).  Returns
+// false if no plan reproduces the reference for every valid q.  Runs on the
+// device at upload (one thread per row) and on the host (same candidates in
+// the same order, so both pick the same plan).
+__host__ __device__ bool build_widen_plan(float alpha, float beta, WidenPlan* out, uint32_t inv[8]) {
+  bool all_invalid = true;
+  for (int i = 0; i < 8; ++i) inv[i] = 0u;
   for (int q = 0; q < 256; ++q) {
-    ref[q] = ref_widen(q, alpha, beta);
-    invalid[q] = ref[q] < 0 || ref[q] >= 32768;
+    const long ref = ref_widen(q, alpha, beta);
+    if (ref < 0 || ref >= 32768) inv[q >> 5] |= 1u << (q & 31);
+    else all_invalid = false;
   }
-  if (!std::isfinite(alpha) || !std::isfinite(beta)) {
-    bool all_invalid = true;
-    for (int q = 0; q < 256; ++q) all_invalid &= invalid[q];
+  if (!isfinite(alpha) || !isfinite(beta)) {
     if (all_invalid) {
       *out = WidenPlan{0, 0, plan_sel(0)};
       return true;
@@ -84,40 +91,115 @@ bool build_widen_plan(float alpha, float beta, WidenPlan* out, bool invalid[256]
   }
   // C = floor((beta + 1/2) * 2^40).  beta*2^40 is exact in double; floor is
   // exact below 2^53 and a no-op above.
-  const int64_t C0 = int64_t(std::floor(std::ldexp(double(beta), 40))) + (int64_t(1) << 39);
-
+  const int64_t C0 = int64_t(floor(ldexp(double(beta), 40))) + (int64_t(1) << 39);
   auto verify = [&](uint32_t M, uint32_t pos, int64_t C) {
-    WidenPlan p{uint64_t(C), M, plan_sel(pos)};
+    const WidenPlan p{uint64_t(C), M, plan_sel(pos)};
     for (int q = 0; q < 256; ++q) {
-      if (invalid[q]) continue;
+      if ((inv[q >> 5] >> (q & 31)) & 1u) continue;
       const uint32_t hi = widen_hi(uint32_t(q), p);
-      if (long(hi >> 8) != ref[q] || hi >= (1u << 23)) return false;
+      if (long(hi >> 8) != ref_widen(q, alpha, beta) || hi >= (1u << 23)) return false;
     }
     *out = p;
     return true;
   };
-
-  // Exact M: alpha * 2^(40 - 8*pos) integral and below 2^32.
-  std::vector<std::pair<uint32_t, uint32_t>> cands;  // (M, pos)
-  for (uint32_t pos : {2u, 1u, 3u, 0u}) {
-    const double Md = std::ldexp(double(alpha), 40 - 8 * int(pos));
-    if (Md >= 0.0 && Md < 4294967296.0 && Md == std::floor(Md)) cands.push_back({uint32_t(Md), pos});
+  // Exact M: alpha * 2^(40 - 8*pos) integral and below 2^32; then rounded M
+  // (tiny or huge alpha), still verified exhaustively.
+  uint32_t cm[8], cp[8];
+  int nc = 0;
+  const uint32_t exact_order[4] = {2u, 1u, 3u, 0u};
+  for (int i = 0; i < 4; ++i) {
+    const double Md = ldexp(double(alpha), 40 - 8 * int(exact_order[i]));
+    if (Md >= 0.0 && Md < 4294967296.0 && Md == floor(Md)) {
+      cm[nc] = uint32_t(Md);
+      cp[nc++] = exact_order[i];
+    }
   }
-  // Approximate M (tiny or huge alpha): rounded, still verified exhaustively.
-  for (uint32_t pos : {0u, 1u, 2u, 3u}) {
-    const double Md = std::ldexp(double(alpha), 40 - 8 * int(pos));
-    if (Md >= 0.0 && Md < 4294967295.5) cands.push_back({uint32_t(std::llround(Md)), pos});
+  for (uint32_t pos = 0; pos < 4; ++pos) {
+    const double Md = ldexp(double(alpha), 40 - 8 * int(pos));
+    if (Md >= 0.0 && Md < 4294967295.5) {
+      cm[nc] = uint32_t(llround(Md));
+      cp[nc++] = pos;
+    }
   }
-  static const int64_t nudges[] = {0,       1,        -1,        256,        -256,
-                                   65536,   -65536,   1 << 24,   -(1 << 24), int64_t(1) << 30,
-                                   -(int64_t(1) << 30), int64_t(1) << 34, -(int64_t(1) << 34)};
-  for (const auto& [M, pos] : cands)
-    for (int64_t d : nudges)
-      if (verify(M, pos, C0 + d)) return true;
+  const int64_t nudges[13] = {0,       1,        -1,        256,        -256,
+                              65536,   -65536,   1 << 24,   -(1 << 24), int64_t(1) << 30,
+                              -(int64_t(1) << 30), int64_t(1) << 34, -(int64_t(1) << 34)};
+  for (int i = 0; i < nc; ++i)
+    for (int k = 0; k < 13; ++k)
+      if (verify(cm[i], cp[i], C0 + nudges[k])) return true;
   return false;
 }
 
+// One thread per row of the device model (padding rows get the inert plan):
+// plans, invalid-q masks, the first row without a plan and the smallest byte
+// position any plan uses.
+__global__ void build_plans(const float* __restrict__ alpha, const float* __restrict__ beta, int64_t rows,
+                            int64_t rp, WidenPlan* __restrict__ plans, uint32_t* __restrict__ invalid,
+                            unsigned long long* __restrict__ fail_row, unsigned int* __restrict__ pos_min) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rp) return;
+  if (r >= rows) {
+    plans[r] = WidenPlan{0, 0, plan_sel(0)};
+    return;
+  }
+  WidenPlan p;
+  uint32_t inv[8];
+  if (build_widen_plan(alpha[r], beta[r], &p, inv)) {
+    plans[r] = p;
+    atomicMin(pos_min, plan_pos(p));
+  } else {
+    plans[r] = WidenPlan{0, 0, plan_sel(0)};
+    atomicMin(fail_row, (unsigned long long)r);
+  }
+  for (int i = 0; i < 8; ++i) invalid[r * 8 + i] = inv[i];
+}
+
 size_t align_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
+
+// Device-side loader: the packed sections, copied to the
+// device as they are in the file, are scattered into the chunk-major record
+// layout (ccq_internal.hpp) here - one warp per (chunk, row) record - instead
+// of a host-side re-layout pass.  2.06 rows also get their widening plan and
+// every stored byte is checked against the row's invalid-q mask (the
+// reference's DomainError, coding.hpp:145-148); the first offending byte in
+// file order wins (atomicMin on its row-major byte offset).
+__global__ void __launch_bounds__(256) relayout_records(
+    const uint8_t* __restrict__ codes, uint64_t row_bytes, const uint8_t* __restrict__ nib, uint64_t nib_g0,
+    const WidenPlan* __restrict__ plans, const uint32_t* __restrict__ invalid, int64_t rows, int64_t rp, int64_t gpr,
+    int payload, uint32_t rec, uint32_t cgb, int nch, uint8_t* __restrict__ dst, unsigned long long* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nrec = int64_t(nch) * rp;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < nrec;
+       w += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int c = int(w / rp);
+    const int64_t r = w - int64_t(c) * rp;
+    uint8_t* d = dst + uint64_t(w) * rec;
+    if (r < rows) {
+      const int64_t g0 = int64_t(c) * kChunk;
+      const int ng = int(gpr - g0 < kChunk ? gpr - g0 : kChunk);
+      const uint64_t so = uint64_t(r) * row_bytes + uint64_t(g0) * payload;
+      const int nbytes = ng * payload;
+      const uint32_t* inv = invalid ? invalid + r * 8 : nullptr;
+      for (int i = lane; i < nbytes; i += 32) {
+        const uint8_t q = codes[so + i];
+        d[i] = q;
+        if (inv && ((inv[q >> 5] >> (q & 31)) & 1u)) atomicMin(bad, (unsigned long long)(so + i));
+      }
+      if (nib) {
+        for (int j = 2 * lane; j < ng; j += 64) {
+          const uint64_t gi = nib_g0 + uint64_t(r) * gpr + g0 + j;
+          uint32_t b = (nib[gi >> 1] >> (4 * (gi & 1))) & 0xFu;
+          if (j + 1 < ng) b |= ((nib[(gi + 1) >> 1] >> (4 * ((gi + 1) & 1))) & 0xFu) << 4;
+          d[cgb + j / 2] = uint8_t(b);
+        }
+      }
+    }
+    if (plans && lane < 4) {  // padding rows carry the inert plan
+      const WidenPlan p = r < rows ? plans[r] : WidenPlan{0, 0, plan_sel(0)};
+      reinterpret_cast<uint32_t*>(d + cgb + (nib ? 16 : 0))[lane] = reinterpret_cast<const uint32_t*>(&p)[lane];
+    }
+  }
+}
 
 }  // namespace
 
@@ -232,75 +314,94 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
                      (geo.embedded_scale ? 0 : (uint64_t(rows) * gpr + 1) / 2) + uint64_t(rows) * 4 +
                      (fc.cluster ? uint64_t(rows) * 8 : 0);
 
-  // Host staging in the chunk-major record layout (ccq_internal.hpp).
+  // Device layout (ccq_internal.hpp): records | super | plans.
   const int64_t rp = m->rows_pad;
   const size_t off_codes = 0;
   const size_t off_super = align_up(off_codes + size_t(m->nch) * size_t(rp) * m->rec, 256);
   const size_t off_plan = align_up(off_super + size_t(rp) * 4, 256);
   const size_t total = align_up(off_plan + (fc.cluster ? size_t(rp) * sizeof(WidenPlan) : 0), 256) + 256;
-  std::vector<uint8_t> host(total, 0);
-  auto rec_at = [&](int c, int64_t r) { return &host[off_codes + (size_t(c) * rp + r) * m->rec]; };
-  for (int64_t r = 0; r < rows; ++r) {
-    const int64_t src = r0 + r;
-    for (int c = 0; c < m->nch; ++c) {
-      const int64_t g0 = int64_t(c) * kChunk;
-      const int64_t ng = std::min<int64_t>(kChunk, gpr - g0);
-      uint8_t* rec = rec_at(c, r);
-      std::memcpy(rec, v->code_payload + uint64_t(src) * row_bytes + uint64_t(g0) * geo.payload_bytes,
-                  size_t(ng) * geo.payload_bytes);
-      if (!geo.embedded_scale) {
-        uint8_t* dst = rec + m->cgb;
-        for (int64_t j = 0; j < ng; ++j) {
-          const uint64_t gi = uint64_t(src) * gpr + g0 + j;
-          const uint8_t nib = (v->scale_payload[gi / 2] >> (4 * (gi % 2))) & 0xF;
-          dst[j / 2] |= uint8_t(nib << (4 * (j % 2)));
-        }
-      }
-    }
-  }
-  if (rows) std::memcpy(&host[off_super], v->super_scales + r0, size_t(rows) * 4);
-  if (fc.cluster) {
-    auto* plans = reinterpret_cast<WidenPlan*>(&host[off_plan]);
-    for (int64_t r = rows; r < rp; ++r) plans[r] = WidenPlan{0, 0, plan_sel(0)};
-    for (int64_t r = 0; r < rows; ++r) {
-      bool invalid[256];
-      const int64_t src = r0 + r;
-      if (!build_widen_plan(v->cluster_scales[src], v->cluster_zero_points[src], &plans[r],
-                            invalid)) {
-        delete m;
-        return fail(CCQ_ERR_DOMAIN, "row " + std::to_string(src) +
-                                        ": cluster parameters have no exact fixed-point "
-                                        "widening plan");
-      }
-      // The reference raises DomainError when it decodes such a byte
-      // (coding.hpp:145-148); we raise it at upload for any stored byte.
-      const uint8_t* row = v->code_payload + uint64_t(src) * row_bytes;
-      for (uint64_t i = 0; i < row_bytes; ++i) {
-        if (invalid[row[i]]) {
-          delete m;
-          return fail(CCQ_ERR_DOMAIN,
-                      "clustered code reconstructs outside [0, 2^15): q=" +
-                          std::to_string(int(row[i])) + " (row " + std::to_string(src) + ")");
-        }
-      }
-    }
-    for (int64_t r = 0; r < rp; ++r)
-      for (int c = 0; c < m->nch; ++c)
-        std::memcpy(rec_at(c, r) + m->cgb + 16, &plans[r], sizeof(WidenPlan));
-    m->plan_pos_min = 3;
-    for (int64_t r = 0; r < rows; ++r) m->plan_pos_min = std::min(m->plan_pos_min, int(plan_pos(plans[r])));
-  }
 
   int prev = 0;
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
+  // Staging: the row range's code bytes and nibbles exactly as stored, the
+  // cluster parameters, invalid-q masks and two result words.
+  const uint64_t code_len = uint64_t(rows) * row_bytes;
+  const uint64_t nib_lo = geo.embedded_scale ? 0 : (uint64_t(r0) * gpr) / 2;
+  const uint64_t nib_hi = geo.embedded_scale ? 0 : (uint64_t(r1) * gpr + 1) / 2;
+  const size_t s_nib = align_up(code_len, 256), s_ab = align_up(s_nib + (nib_hi - nib_lo), 256);
+  const size_t s_inv = align_up(s_ab + (fc.cluster ? size_t(rows) * 8 : 0), 256);
+  const size_t s_res = align_up(s_inv + (fc.cluster ? size_t(rows) * 32 : 0), 256), s_total = s_res + 256;
+  uint8_t* stage = nullptr;
+  // res[0]: first offending byte offset, res[1]: first row without a plan, res[2] (u32): min plan byte position
+  unsigned long long res[3] = {~0ull, ~0ull, 3ull};
+  WidenPlan* dplans = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&m->base, total);
-  if (e == cudaSuccess) e = cudaMemcpy(m->base, host.data(), total, cudaMemcpyHostToDevice);
-  cudaSetDevice(prev);
+  if (e == cudaSuccess) {
+    dplans = fc.cluster ? reinterpret_cast<WidenPlan*>(static_cast<uint8_t*>(m->base) + off_plan) : nullptr;
+    e = cudaMalloc(&stage, s_total);
+  }
+  if (e == cudaSuccess) e = cudaMemset(m->base, 0, total);
+  if (e == cudaSuccess && code_len)
+    e = cudaMemcpy(stage, v->code_payload + uint64_t(r0) * row_bytes, code_len, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && nib_hi > nib_lo)
+    e = cudaMemcpy(stage + s_nib, v->scale_payload + nib_lo, nib_hi - nib_lo, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && rows)
+    e = cudaMemcpy(static_cast<uint8_t*>(m->base) + off_super, v->super_scales + r0, size_t(rows) * 4,
+                   cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && fc.cluster && rows) {
+    e = cudaMemcpy(stage + s_ab, v->cluster_scales + r0, size_t(rows) * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(stage + s_ab + size_t(rows) * 4, v->cluster_zero_points + r0, size_t(rows) * 4,
+                     cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(stage + s_res, res, sizeof(res), cudaMemcpyHostToDevice);
+  int64_t plan_fail = rows;  // first row without an exact plan
+  if (e == cudaSuccess && fc.cluster && rp > 0) {
+    build_plans<<<unsigned((rp + 127) / 128), 128>>>(
+        reinterpret_cast<const float*>(stage + s_ab), reinterpret_cast<const float*>(stage + s_ab) + rows, rows, rp,
+        dplans, reinterpret_cast<uint32_t*>(stage + s_inv), reinterpret_cast<unsigned long long*>(stage + s_res) + 1,
+        reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(stage + s_res) + 2));
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(res, stage + s_res, sizeof(res), cudaMemcpyDeviceToHost);
+    if (res[1] != ~0ull) plan_fail = int64_t(res[1]);
+    m->plan_pos_min = int(uint32_t(res[2]));
+  }
+  unsigned long long bad = ~0ull;
+  if (e == cudaSuccess && m->nch > 0 && rp > 0) {
+    const int64_t warps = int64_t(m->nch) * rp;
+    const unsigned blocks = unsigned(std::min<int64_t>((warps + 7) / 8, int64_t(num_sms(device)) * 16));
+    relayout_records<<<blocks, 256>>>(
+        stage, row_bytes, geo.embedded_scale ? nullptr : stage + s_nib, uint64_t(r0) * gpr - 2 * nib_lo, dplans,
+        fc.cluster ? reinterpret_cast<const uint32_t*>(stage + s_inv) : nullptr, std::min(rows, plan_fail), rp, gpr,
+        geo.payload_bytes, m->rec, m->cgb, m->nch, static_cast<uint8_t*>(m->base) + off_codes,
+        reinterpret_cast<unsigned long long*>(stage + s_res));
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(&bad, stage + s_res, sizeof(bad), cudaMemcpyDeviceToHost);
+  }
+  if (stage) cudaFree(stage);
   if (e != cudaSuccess) {
     if (m->base) cudaFree(m->base);
+    cudaSetDevice(prev);
     delete m;
     return cuda_fail(e, "model upload");
+  }
+  cudaSetDevice(prev);
+  // Errors in file order: a stored byte the reference rejects (coding.hpp:145-148;
+  // we raise it at upload for any stored byte), or a row without an exact plan.
+  const int64_t bad_row = bad == ~0ull ? rows : int64_t(bad / row_bytes);
+  if (bad_row < rows && bad_row <= plan_fail) {
+    const uint8_t q = v->code_payload[uint64_t(r0) * row_bytes + bad];
+    cudaFree(m->base);
+    delete m;
+    return fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^15): q=" + std::to_string(int(q)) +
+                                    " (row " + std::to_string(r0 + bad_row) + ")");
+  }
+  if (plan_fail < rows) {
+    cudaFree(m->base);
+    delete m;
+    return fail(CCQ_ERR_DOMAIN, "row " + std::to_string(r0 + plan_fail) +
+                                    ": cluster parameters have no exact fixed-point widening plan");
   }
   auto* b = static_cast<uint8_t*>(m->base);
   m->device_bytes = total;
