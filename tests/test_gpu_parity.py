@@ -630,3 +630,22 @@ def test_device_loader_multi_chunk_rows(oracle, ccq, cuda, fam):
     assert np.array_equal(w.cpu().numpy().view(np.uint32), oracle.dequantize(s).view(np.uint32))
     x = oracle.random_matrix(3, 64 * 70, "gaussian", 6)
     assert rel_err(ccq.gemv_batch(d, x), oracle.gemv_batch(s, x)) < REL_TOL
+
+
+@pytest.mark.parametrize("M", [3, 5, 8])
+def test_k_heavy_206_small_batch_on_gemm(oracle, ccq, cuda, M):
+    """2.06 on a K-heavy layer (14336 -> 4096) hands M >= 3 to the split-K
+    tcgen05 GEMM (model.cu dispatch): whole output against the tensor-pipe
+    GEMV and sampled rows against the oracle."""
+    torch = cuda
+    s = oracle.random_packed(4096, 14336, 2, 64, seed=14336 + M)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = bf16_round(oracle.random_matrix(M, 14336, "gaussian", 200 + M))
+    xt = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+    y = ccq.matmul(d, xt)
+    ref = ccq.matmul(d, xt, kernel="gemv")
+    torch.cuda.synchronize()
+    assert rel_err(y.cpu().numpy(), ref.cpu().numpy()) < REL_TOL
+    for r0, r1 in ((0, 16), (4080, 4096)):
+        want = oracle.gemv_batch(_slice_rows(oracle, s, r0, r1), x, threads=8)
+        assert rel_err(y[:, r0:r1].cpu().numpy(), want) < REL_TOL
