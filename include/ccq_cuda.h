@@ -201,6 +201,18 @@ int ccq_clustered_code_value(uint8_t q, float alpha, float beta, int32_t code_bi
 /* Number of kernels this library launched since load (bench accounting). */
 uint64_t ccq_cuda_launch_count(void);
 
+/* Exhaustive trellis code search of the CCQ quantizer for n subvectors
+ * (replaces ccq::search_codes, core/src/quantizer.cpp:36-103, one call per
+ * subvector; bit-identical codes).  Device pointers: targets[n][stride] f32
+ * (the first `valid` values of each row are the subvector), scales[n] f64,
+ * codes[n] out.  Config = EncodingConfig (state_bits L, states_per_code N,
+ * transition_bits S), validated like EncodingConfig::validate
+ * (CCQ_ERR_CONFIG); valid outside 1..N is CCQ_ERR_SHAPE as in the reference. */
+int ccq_cuda_search_codes(const float* targets, int64_t n, int32_t valid, int32_t stride,
+                          const double* scales, int32_t zero_point, int32_t state_bits,
+                          int32_t states_per_code, int32_t transition_bits, uint32_t* codes,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -262,6 +262,7 @@ def ref():
                                                  C.c_size_t, vp, C.c_size_t, vp, vp, vp,
                                                  C.POINTER(vp)]
         L.ccqref_load_model.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.ccqref_search_codes.argtypes = [vp, i64, C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.ccqref_write_container.argtypes = [vp, C.c_char_p]
         L.ccqref_model_shape.argtypes = [vp] + [C.POINTER(i64)] * 2 + [C.POINTER(C.c_int)] * 3 \
             + [C.POINTER(u64)] * 3

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <span>
 #include <string>
 #include <thread>
 #include <vector>
@@ -161,6 +162,22 @@ int ccqref_model_from_sections(std::int64_t rows, std::int64_t cols, int family,
       m->cluster_zero_points.assign(czp, czp + rows);
     }
     *out = m;
+  });
+}
+
+// ccq::search_codes (quantizer.cpp:36-103) over n subvectors: targets[i] holds
+// `valid` floats (row stride `stride`), scales[i] the group scale.
+int ccqref_search_codes(const float* targets, std::int64_t n, int valid, int stride, const double* scales,
+                        int zero_point, int state_bits, int states_per_code, int transition_bits,
+                        std::uint32_t* codes) {
+  return guard([&] {
+    ccq::EncodingConfig cfg;
+    cfg.state_bits = state_bits;
+    cfg.states_per_code = states_per_code;
+    cfg.transition_bits = transition_bits;
+    for (std::int64_t i = 0; i < n; ++i)
+      codes[i] = ccq::search_codes(std::span<const float>(targets + i * stride, std::size_t(valid)), scales[i],
+                                   zero_point, cfg);
   });
 }
 

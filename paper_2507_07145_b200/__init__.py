@@ -32,7 +32,7 @@ __all__ = [
     "CcqError", "ConfigError", "DomainError", "ShapeError", "EncodingError", "FormatError",
     "CudaError", "FAMILIES", "PackedModel", "DeviceModel", "load_model", "dequantize", "gemv",
     "gemv_batch", "model_payload_bytes", "group_geometry", "clustered_code_value", "decode",
-    "matmul", "grouped", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
+    "matmul", "grouped", "search_codes", "ENCODINGS", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
     "moe_forward",
 ]
 
@@ -102,7 +102,7 @@ ABI_SYMBOLS = [
     "ccq_cuda_gemv", "ccq_cuda_gemm", "ccq_cuda_grouped", "ccq_dequantize_host",
     "ccq_gemv_host", "ccq_gemv_batch_host", "ccq_model_payload_bytes", "ccq_group_geometry",
     "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
-    "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward",
+    "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward", "ccq_cuda_search_codes",
 ]
 
 _lib = None
@@ -136,6 +136,7 @@ def lib():
         L.ccq_cuda_experts_upload.argtypes = [vp, i32, C.c_int, C.POINTER(vp)]
         L.ccq_cuda_experts_matmul.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_cuda_moe_forward.argtypes = [vp, vp, vp, i64, i32, vp, C.c_int, vp, C.c_int, vp]
+        L.ccq_cuda_search_codes.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i32, vp, vp]
         L.ccq_dequantize_host.argtypes = [vp, vp]
         L.ccq_gemv_host.argtypes = [vp, vp, u64, vp, u64]
         L.ccq_gemv_batch_host.argtypes = [vp, vp, i64, i64, vp, i64, i64]
@@ -441,6 +442,32 @@ def moe_forward(experts: "Experts", topk_ids, topk_weights, x, out=None, out_dty
                                       topk_ids.shape[1], x.data_ptr(), _torch_dtype_code(x), out.data_ptr(),
                                       _torch_dtype_code(out), _stream_ptr(stream)))
     return out
+
+
+# EncodingConfig (state_bits L, states_per_code N, transition_bits S) of each
+# family's code parts (coding.cpp:24-27): 2.75, 2.06, and the 2.5 hybrid's two parts.
+ENCODINGS = {"2.75": (4, 3, 2), "2.06": (6, 4, 3), "2.5-high": (3, 3, 2), "2.5-low": (3, 4, 2)}
+
+
+def search_codes(targets, scales, config, zero_point=None, valid=None, stream=None):
+    """Quantizer step on the GPU (ccq_cuda_search_codes): the reference's
+    search_codes (quantizer.cpp:36-103) for every row of targets[n, >=valid]
+    (f32, CUDA) with scales[n] (f64, CUDA) -> int32 codes[n], bit-identical.
+    zero_point defaults to 2^(L-1) (the family schemes' zero point)."""
+    import torch
+    L, N, S = config
+    if zero_point is None:
+        zero_point = 1 << (L - 1)
+    if targets.dim() != 2 or targets.dtype != torch.float32 or scales.dtype != torch.float64:
+        raise ShapeError("targets must be [n, k] float32 and scales float64")
+    if not (targets.is_contiguous() and scales.is_contiguous()) or scales.numel() != targets.shape[0]:
+        raise ShapeError("targets / scales must be contiguous with one scale per row")
+    valid = targets.shape[1] if valid is None else valid
+    codes = torch.empty(targets.shape[0], dtype=torch.int32, device=targets.device)
+    _check(lib().ccq_cuda_search_codes(targets.data_ptr(), targets.shape[0], valid, targets.shape[1],
+                                       scales.data_ptr(), zero_point, L, N, S, codes.data_ptr(),
+                                       _stream_ptr(stream)))
+    return codes
 
 
 def grouped(models, offsets, x, out=None, out_dtype=None, stream=None):
