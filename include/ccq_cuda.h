@@ -213,6 +213,18 @@ int ccq_cuda_search_codes(const float* targets, int64_t n, int32_t valid, int32_
                           int32_t states_per_code, int32_t transition_bits, uint32_t* codes,
                           void* stream);
 
+/* The CCQ quantizer on the GPU: pack_model(quantize_tensor(W)) (replaces
+ * ccq::quantize_tensor, core/src/quantizer.cpp:319-425, + ccq::pack_model,
+ * container.cpp:323-358), bit-identical sections.  Host buffers: w[rows][cols]
+ * f32 in; out: code_payload (groups x payload_bytes), scale_payload
+ * ((groups+1)/2 bytes, families with side-band scales, else may be NULL),
+ * super_scales[rows], cluster_scales / cluster_zero_points [rows] (2.06,
+ * else may be NULL).  Per-group search + refinement and the 2.06 cluster
+ * re-search run on `device`.  group_size <= 256. */
+int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size,
+                      int32_t rounds, int32_t device, uint8_t* code_payload, uint8_t* scale_payload,
+                      float* super_scales, float* cluster_scales, float* cluster_zero_points);
+
 #ifdef __cplusplus
 }
 #endif

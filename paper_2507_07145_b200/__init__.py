@@ -32,7 +32,7 @@ __all__ = [
     "CcqError", "ConfigError", "DomainError", "ShapeError", "EncodingError", "FormatError",
     "CudaError", "FAMILIES", "PackedModel", "DeviceModel", "load_model", "dequantize", "gemv",
     "gemv_batch", "model_payload_bytes", "group_geometry", "clustered_code_value", "decode",
-    "matmul", "grouped", "search_codes", "ENCODINGS", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
+    "matmul", "grouped", "search_codes", "quantize", "ENCODINGS", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
     "moe_forward",
 ]
 
@@ -103,6 +103,7 @@ ABI_SYMBOLS = [
     "ccq_gemv_host", "ccq_gemv_batch_host", "ccq_model_payload_bytes", "ccq_group_geometry",
     "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
     "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward", "ccq_cuda_search_codes",
+    "ccq_quantize_host",
 ]
 
 _lib = None
@@ -137,6 +138,7 @@ def lib():
         L.ccq_cuda_experts_matmul.argtypes = [vp, vp, vp, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_cuda_moe_forward.argtypes = [vp, vp, vp, i64, i32, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_cuda_search_codes.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i32, vp, vp]
+        L.ccq_quantize_host.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.ccq_dequantize_host.argtypes = [vp, vp]
         L.ccq_gemv_host.argtypes = [vp, vp, u64, vp, u64]
         L.ccq_gemv_batch_host.argtypes = [vp, vp, i64, i64, vp, i64, i64]
@@ -468,6 +470,28 @@ def search_codes(targets, scales, config, zero_point=None, valid=None, stream=No
                                        scales.data_ptr(), zero_point, L, N, S, codes.data_ptr(),
                                        _stream_ptr(stream)))
     return codes
+
+
+def quantize(weights, family, group_size: int = 64, rounds: int = 2, device: int = 0) -> PackedModel:
+    """pack_model(quantize_tensor(W)) with the search on the GPU
+    (ccq_quantize_host): W[rows, cols] f32 (host) -> PackedModel whose
+    sections are bit-identical to the reference quantizer's."""
+    w = np.ascontiguousarray(weights, np.float32)
+    if w.ndim != 2:
+        raise ShapeError("weights must be a 2-D matrix")
+    fam = FAMILIES[family] if isinstance(family, str) else int(family)
+    rows, cols = w.shape
+    geo = group_geometry(fam, group_size)
+    groups = rows * (cols // group_size) if group_size > 0 else 0
+    code = np.zeros(groups * geo["payload_bytes"], np.uint8)
+    scale = np.zeros(0 if geo["embedded_scale"] else (groups + 1) // 2, np.uint8)
+    sup = np.zeros(rows, np.float32)
+    cl = fam == FAMILIES["2.06"]
+    cs = np.zeros(rows if cl else 0, np.float32)
+    czp = np.zeros(rows if cl else 0, np.float32)
+    _check(lib().ccq_quantize_host(_np_ptr(w), rows, cols, fam, group_size, rounds, device, _np_ptr(code),
+                                   _np_ptr(scale), _np_ptr(sup), _np_ptr(cs), _np_ptr(czp)))
+    return PackedModel(rows, cols, fam, group_size, code, scale, sup, cs, czp, rounds)
 
 
 def grouped(models, offsets, x, out=None, out_dtype=None, stream=None):

@@ -14,7 +14,10 @@
 // (__dmul_rn/__dsub_rn/__dadd_rn): no FMA contraction, as in the reference's
 // x86-64 build.
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "ccq_internal.hpp"
 
@@ -69,6 +72,205 @@ __global__ void __launch_bounds__(256) search_codes_kernel(const float* __restri
   }
 }
 
+
+// ---- the whole quantizer (quantize_tensor, quantizer.cpp:319-425) ----------
+
+constexpr int kQWarps = 8;    // warps (groups in flight) per CTA
+constexpr int kQMaxGS = 256;  // largest group size the GPU quantizer takes
+
+// Family scheme (coding.cpp:24-27, 213-249): code parts, word layout.
+struct QScheme {
+  int nparts, L[2], N[2], S[2];
+  int code_bits, wpw, zp, sb, gs, full_words, has_tail, words;
+  uint32_t wmask;
+  int shifts[8];
+};
+
+// search_codes for one subvector, the whole warp cooperating (see
+// search_codes_kernel); tab holds valid x 2^L doubles.  All lanes return the code.
+__device__ uint32_t warp_search(const float* tgt, int valid, double scale, int zp, int L, int N, int S,
+                                double* tab) {
+  const int lane = threadIdx.x & 31, nst = 1 << L;
+  __syncwarp();
+  for (int e = lane; e < valid * nst; e += 32) {
+    const int j = e / nst, st = e - j * nst;
+    const double d = __dsub_rn(double(tgt[j]), __dmul_rn(double(st - zp), scale));
+    tab[e] = __dmul_rn(d, d);
+  }
+  __syncwarp();
+  const uint32_t smask = uint32_t(nst - 1), fmask = (1u << S) - 1u;
+  const uint32_t nleaf = 1u << (L + (valid - 1) * S);
+  double best = __longlong_as_double(0x7FF0000000000000LL);
+  uint32_t bcode = 0;
+  for (uint32_t leaf = lane; leaf < nleaf; leaf += 32) {
+    uint32_t st = leaf >> ((valid - 1) * S);
+    double acc = tab[st];
+    for (int j = 1; j < valid; ++j) {
+      st = ((st << S) | ((leaf >> ((valid - 1 - j) * S)) & fmask)) & smask;
+      acc = __dadd_rn(acc, tab[j * nst + st]);
+    }
+    if (acc < best) {
+      best = acc;
+      bcode = leaf;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const uint32_t oc = __shfl_xor_sync(0xffffffffu, bcode, off);
+    if (ob < best || (ob == best && oc < bcode)) {
+      best = ob;
+      bcode = oc;
+    }
+  }
+  __syncwarp();
+  return bcode << ((N - valid) * S);
+}
+
+// search_group (quantizer.cpp:157-170) -> words[], then the decoded states
+// (decode_group_states, quantizer.cpp:120-133) and group_error (172-180;
+// sequential sum on lane 0).  Returns the error on every lane.
+__device__ double search_and_score(const QScheme& q, const float* g, double scale, uint16_t* words, int* st,
+                                   double* tab) {
+  const int lane = threadIdx.x & 31;
+  for (int w = 0; w < q.words; ++w) {
+    const bool tail = w == q.full_words;
+    const float* tg = tail ? g + q.gs - 1 : g + w * q.wpw;
+    const int len = tail ? 1 : q.wpw;
+    uint32_t word = 0;
+    int bits_left = q.code_bits, offset = 0;
+    for (int p = 0; p < q.nparts; ++p) {
+      bits_left -= q.L[p] + (q.N[p] - 1) * q.S[p];
+      const int take = q.N[p] < len - offset ? q.N[p] : len - offset;
+      const uint32_t code = warp_search(tg + offset, take, scale, q.zp, q.L[p], q.N[p], q.S[p], tab);
+      word |= code << bits_left;
+      offset += take;
+      if (offset == len) break;
+    }
+    if (lane == 0) words[w] = uint16_t(word);
+  }
+  __syncwarp();
+  for (int i = lane; i < q.gs; i += 32) st[i] = int((words[i / q.wpw] >> q.shifts[i % q.wpw]) & q.wmask);
+  __syncwarp();
+  double err = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < q.gs; ++i) {
+      const double d = __dsub_rn(double(g[i]), __dmul_rn(double(st[i] - q.zp), scale));
+      err = __dadd_rn(err, __dmul_rn(d, d));
+    }
+  return __shfl_sync(0xffffffffu, err, 0);
+}
+
+__device__ double group_err(const QScheme& q, const float* g, const int* st, double scale) {
+  double err = 0.0;
+  if ((threadIdx.x & 31) == 0)
+    for (int i = 0; i < q.gs; ++i) {
+      const double d = __dsub_rn(double(g[i]), __dmul_rn(double(st[i] - q.zp), scale));
+      err = __dadd_rn(err, __dmul_rn(d, d));
+    }
+  return __shfl_sync(0xffffffffu, err, 0);
+}
+
+// quantize_group (quantizer.cpp:183-222) for every group: one warp per group.
+// Outputs the best code words and the raw (pre-snapping) scale as float.
+__global__ void __launch_bounds__(kQWarps * 32) quantize_groups(const float* __restrict__ W, int64_t rows,
+                                                               int64_t cols, QScheme q, int rounds,
+                                                               uint16_t* __restrict__ words_out,
+                                                               float* __restrict__ scale_out) {
+  __shared__ float gsh[kQWarps][kQMaxGS];
+  __shared__ int stsh[kQWarps][kQMaxGS];
+  __shared__ uint16_t cur[kQWarps][kQMaxGS / 3 + 2], best_w[kQWarps][kQMaxGS / 3 + 2];
+  __shared__ double tab[kQWarps][256];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t gpr = cols / q.gs, groups = rows * gpr;
+  float* g = gsh[wib];
+  int* st = stsh[wib];
+  for (int64_t gi = int64_t(blockIdx.x) * kQWarps + wib; gi < groups; gi += int64_t(gridDim.x) * kQWarps) {
+    const float* src = W + (gi / gpr) * cols + (gi % gpr) * q.gs;
+    double mx = 0.0;
+    for (int i = lane; i < q.gs; i += 32) {
+      g[i] = src[i];
+      mx = fmax(mx, fabs(double(g[i])));  // init_group_scale (quantizer.cpp:29-34); NaN ignored like std::max
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    __syncwarp();
+    double scale = __ddiv_rn(mx, double((1 << (q.sb - 1)) - 1));
+    double err = search_and_score(q, g, scale, cur[wib], st, tab[wib]);
+    double bscale = scale, berr = err;
+    for (int w = lane; w < q.words; w += 32) best_w[wib][w] = cur[wib][w];
+    for (int round = 1; round <= rounds; ++round) {
+      // optimize_scale (quantizer.cpp:105-118) on the current states, lane 0
+      double ns = 0.0;
+      if (lane == 0) {
+        double num = 0.0, den = 0.0;
+        for (int i = 0; i < q.gs; ++i) {
+          const double c = double(st[i] - q.zp);
+          num = __dadd_rn(num, __dmul_rn(double(g[i]), c));
+          den = __dadd_rn(den, __dmul_rn(c, c));
+        }
+        ns = den == 0.0 ? scale : __ddiv_rn(num, den);
+      }
+      ns = __shfl_sync(0xffffffffu, ns, 0);
+      scale = 0.0 < ns ? ns : 0.0;  // std::max(0.0, x)
+      err = group_err(q, g, st, scale);
+      if (err < berr) {
+        __syncwarp();
+        for (int w = lane; w < q.words; w += 32) best_w[wib][w] = cur[wib][w];
+        bscale = scale;
+        berr = err;
+      }
+      if (round < rounds) {
+        err = search_and_score(q, g, scale, cur[wib], st, tab[wib]);
+        if (err < berr) {
+          __syncwarp();
+          for (int w = lane; w < q.words; w += 32) best_w[wib][w] = cur[wib][w];
+          bscale = scale;
+          berr = err;
+        }
+      }
+    }
+    __syncwarp();
+    for (int w = lane; w < q.words; w += 32) words_out[gi * q.words + w] = best_w[wib][w];
+    if (lane == 0) scale_out[gi] = float(bscale);
+    __syncwarp();
+  }
+}
+
+// 2.06 cluster-aware re-search (quantizer.cpp:392-409, search_cluster_table
+// 272-291): one thread per subvector, the row's 256-entry table.
+__global__ void cluster_research(const float* __restrict__ W, int64_t rows, int64_t cols, QScheme q,
+                                 const float* __restrict__ group_scales, const uint8_t* __restrict__ tstates,
+                                 const uint16_t* __restrict__ tcodes, uint8_t* __restrict__ clustered,
+                                 uint16_t* __restrict__ words) {
+  const int64_t gpr = cols / q.gs, n = rows * gpr * q.words;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t gi = i / q.words, r = gi / gpr;
+    const int w = int(i - gi * q.words);
+    const bool tail = q.has_tail && w == q.full_words;
+    const float* g = W + r * cols + (gi % gpr) * q.gs;
+    const float* t = tail ? g + q.gs - 1 : g + w * q.wpw;
+    const int valid = tail ? 1 : q.wpw;
+    const double scale = double(group_scales[gi]);
+    const uint8_t* ts = tstates + r * 256 * 8;
+    double best = __longlong_as_double(0x7FF0000000000000LL);
+    int bq = 0;
+    for (int c = 0; c < 256; ++c) {
+      double cost = 0.0;
+      for (int j = 0; j < valid; ++j) {
+        const double d = __dsub_rn(double(t[j]), __dmul_rn(double(int(ts[c * 8 + j]) - q.zp), scale));
+        cost = __dadd_rn(cost, __dmul_rn(d, d));
+      }
+      if (cost < best) {
+        best = cost;
+        bq = c;
+      }
+    }
+    clustered[i] = uint8_t(bq);
+    words[i] = tcodes[r * 256 + bq];
+  }
+}
+
 }  // namespace
 }  // namespace ccqb
 
@@ -104,4 +306,160 @@ extern "C" int ccq_cuda_search_codes(const float* targets, int64_t n, int32_t va
   count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "search_codes launch");
+}
+
+// ---- quantize_tensor + pack_model on the GPU (host driver) -----------------
+// Per-group search and refinement (quantize_groups) and the 2.06 cluster
+// re-search (cluster_research) run on the device; the per-row O(groups)
+// steps - scale snapping (quantize_scales, packing.cpp:142-158), the code
+// cluster range (cluster_channel, quantizer.cpp:224-247), the 256-entry
+// cluster tables (build_cluster_table, 258-270) and byte packing
+// (pack_group / pack_cluster_scales, packing.cpp:71-114, 160-170) - on the host.
+extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size,
+                                 int32_t rounds, int32_t device, uint8_t* code_payload, uint8_t* scale_payload,
+                                 float* super_scales, float* cluster_scales, float* cluster_zero_points) {
+  Geometry geo;
+  int st = geometry_for(family, group_size, &geo);  // ConfigError as group_geometry
+  if (st != CCQ_OK) return st;
+  if (rounds < 0) return fail(CCQ_ERR_CONFIG, "refinement rounds must be >= 0");
+  if (rows < 0 || cols < 0) return fail(CCQ_ERR_SHAPE, "negative shape");
+  if (cols % group_size != 0)
+    return fail(CCQ_ERR_SHAPE, "input dimension " + std::to_string(cols) + " is not a multiple of group size " +
+                                   std::to_string(group_size));
+  if (group_size > kQMaxGS) return fail(CCQ_ERR_CONFIG, "the GPU quantizer takes group sizes up to 256");
+  const FamilyConst fc = family_const(family);
+  QScheme q{};
+  if (family == kF275) {
+    q.nparts = 1; q.L[0] = 4; q.N[0] = 3; q.S[0] = 2;
+  } else if (family == kF25) {
+    q.nparts = 2; q.L[0] = 3; q.N[0] = 3; q.S[0] = 2; q.L[1] = 3; q.N[1] = 4; q.S[1] = 2;
+  } else {
+    q.nparts = 1; q.L[0] = 6; q.N[0] = 4; q.S[0] = 3;
+  }
+  q.code_bits = fc.code_bits; q.wpw = fc.wpw; q.zp = fc.zero_point; q.sb = fc.state_bits; q.gs = group_size;
+  q.full_words = geo.full_words; q.has_tail = geo.has_tail; q.words = geo.words_per_group; q.wmask = fc.weight_mask;
+  for (int i = 0; i < 8; ++i) q.shifts[i] = i < 7 ? fc.shifts[i] : 0;
+  const int64_t gpr = cols / group_size, groups = rows * gpr, nw = groups * q.words;
+  if (groups == 0) {
+    for (int64_t r = 0; r < rows; ++r) super_scales[r] = 1.0f;
+    return CCQ_OK;
+  }
+  if (!w || !code_payload || !super_scales) return fail(CCQ_ERR_INVALID, "null pointer");
+
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  float *dW = nullptr, *draw = nullptr, *dgs = nullptr;
+  uint16_t *dwords = nullptr, *dtcodes = nullptr;
+  uint8_t *dts = nullptr, *dcl = nullptr;
+  std::vector<uint16_t> words(size_t(nw), 0);
+  std::vector<float> raw(static_cast<size_t>(groups));
+  std::vector<uint16_t> scode(static_cast<size_t>(groups));
+  std::vector<float> gscale(static_cast<size_t>(groups));
+  std::vector<uint8_t> clustered(fc.cluster ? size_t(nw) : 0);
+  auto cleanup = [&] {
+    cudaFree(dW); cudaFree(draw); cudaFree(dgs); cudaFree(dwords); cudaFree(dtcodes); cudaFree(dts); cudaFree(dcl);
+    cudaSetDevice(prev);
+  };
+  if (e == cudaSuccess) e = cudaMalloc(&dW, size_t(rows * cols) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&draw, size_t(groups) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dwords, size_t(nw) * 2);
+  if (e == cudaSuccess) e = cudaMemcpy(dW, w, size_t(rows * cols) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const int64_t blocks = std::min<int64_t>((groups + kQWarps - 1) / kQWarps, int64_t(num_sms(device)) * 8);
+    quantize_groups<<<unsigned(blocks), kQWarps * 32>>>(dW, rows, cols, q, rounds, dwords, draw);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(words.data(), dwords, size_t(nw) * 2, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(raw.data(), draw, size_t(groups) * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "gpu quantizer");
+  }
+  // quantize_scales per row (packing.cpp:142-158)
+  const uint32_t levels = (1u << fc.scale_bits) - 1u;
+  for (int64_t r = 0; r < rows; ++r) {
+    float mx = 0.0f;
+    for (int64_t j = 0; j < gpr; ++j) {
+      const float sv = raw[size_t(r * gpr + j)];
+      if (sv < 0.0f || std::isnan(sv)) {
+        cleanup();
+        return fail(CCQ_ERR_DOMAIN, "group scales must be non-negative");
+      }
+      mx = std::max(mx, sv);
+    }
+    const float sup = mx == 0.0f ? 1.0f : float(double(mx) / double(levels));
+    super_scales[r] = sup;
+    for (int64_t j = 0; j < gpr; ++j) {
+      const long c = std::lround(double(raw[size_t(r * gpr + j)]) / double(sup));
+      const uint16_t code = uint16_t(std::clamp<long>(c, 0, long(levels)));
+      scode[size_t(r * gpr + j)] = code;
+      gscale[size_t(r * gpr + j)] = float(code) * sup;
+    }
+  }
+  if (fc.cluster) {
+    // cluster_channel + build_cluster_table per row, re-search on the device
+    std::vector<uint8_t> tstates(size_t(rows) * 256 * 8, 0);
+    std::vector<uint16_t> tcodes(size_t(rows) * 256);
+    for (int64_t r = 0; r < rows; ++r) {
+      const uint16_t* rw = words.data() + size_t(r * gpr * q.words);
+      uint16_t lo = rw[0], hi = rw[0];
+      for (int64_t i = 0; i < gpr * q.words; ++i) {
+        lo = std::min(lo, rw[i]);
+        hi = std::max(hi, rw[i]);
+      }
+      const float czp = float(lo);
+      const float cs = hi == lo ? 1.0f : float((double(hi) - double(lo)) / 255.0);
+      cluster_scales[r] = cs;
+      cluster_zero_points[r] = czp;
+      for (int c = 0; c < 256; ++c) {
+        const long v = std::lround(double(c) * double(cs) + double(czp));
+        if (v < 0 || v >= (1l << fc.code_bits)) {
+          cleanup();
+          return fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^" + std::to_string(fc.code_bits) +
+                                          "): q=" + std::to_string(c));
+        }
+        tcodes[size_t(r * 256 + c)] = uint16_t(v);
+        for (int j = 0; j < fc.wpw; ++j)
+          tstates[size_t((r * 256 + c) * 8 + j)] = uint8_t((uint32_t(v) >> fc.shifts[j]) & fc.weight_mask);
+      }
+    }
+    e = cudaMalloc(&dgs, size_t(groups) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&dts, tstates.size());
+    if (e == cudaSuccess) e = cudaMalloc(&dtcodes, tcodes.size() * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&dcl, size_t(nw));
+    if (e == cudaSuccess) e = cudaMemcpy(dgs, gscale.data(), size_t(groups) * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dts, tstates.data(), tstates.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dtcodes, tcodes.data(), tcodes.size() * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      const int64_t blocks = std::min<int64_t>((nw + 255) / 256, int64_t(num_sms(device)) * 16);
+      cluster_research<<<unsigned(blocks), 256>>>(dW, rows, cols, q, dgs, dts, dtcodes, dcl, dwords);
+      count_launch();
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(clustered.data(), dcl, size_t(nw), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "gpu quantizer (cluster re-search)");
+    }
+  }
+  cleanup();
+  // pack_model (container.cpp:323-358): payload words little-endian, tail
+  // word carries the scale code (embedded families), side-band nibbles.
+  uint8_t* out = code_payload;
+  for (int64_t gi = 0; gi < groups; ++gi) {
+    for (int wd = 0; wd < q.words; ++wd) {
+      uint32_t v = fc.cluster ? clustered[size_t(gi * q.words + wd)] : words[size_t(gi * q.words + wd)];
+      if (geo.has_tail && wd == q.full_words && !fc.cluster) v |= scode[size_t(gi)];
+      *out++ = uint8_t(v & 0xFF);
+      if (fc.word_bytes == 2) *out++ = uint8_t(v >> 8);
+    }
+  }
+  if (!geo.embedded_scale) {
+    if (!scale_payload) return fail(CCQ_ERR_INVALID, "null scale payload");
+    std::memset(scale_payload, 0, size_t((groups + 1) / 2));
+    for (int64_t gi = 0; gi < groups; ++gi) scale_payload[gi / 2] |= uint8_t(scode[size_t(gi)] << (4 * (gi % 2)));
+  }
+  return CCQ_OK;
 }

@@ -70,3 +70,59 @@ def test_search_codes_errors(ccq, cuda):
         ccq.search_codes(t, s, (4, 3, 2))   # 4 values > N = 3
     with pytest.raises(ccq.ShapeError):
         ccq.search_codes(t, s, (4, 3, 2), valid=0)
+
+
+def _sections_equal(a, b):
+    assert a.rows == b.rows and a.cols == b.cols and a.family == b.family and a.group_size == b.group_size
+    assert np.array_equal(np.asarray(a.code_payload, np.uint8), np.asarray(b.code_payload, np.uint8)), "codes"
+    assert np.array_equal(np.asarray(a.scale_payload, np.uint8), np.asarray(b.scale_payload, np.uint8)), "scales"
+    for x, y, what in ((a.super_scales, b.super_scales, "super"), (a.cluster_scales, b.cluster_scales, "cs"),
+                       (a.cluster_zero_points, b.cluster_zero_points, "czp")):
+        assert np.array_equal(np.asarray(x, np.float32).view(np.uint32), np.asarray(y, np.float32).view(np.uint32)), what
+
+
+@pytest.mark.parametrize("fam,gs,rounds", [(0, 64, 2), (1, 64, 2), (2, 64, 2), (2, 64, 0), (0, 66, 1),
+                                           (2, 65, 2), (1, 57, 3), (0, 64, 0)])
+def test_gpu_quantizer_packed_sections_bit_exact(oracle, ccq, cuda, fam, gs, rounds):
+    """ccq_quantize_host == the reference's pack_model(quantize_tensor(W))
+    byte for byte (codes, side-band nibbles, super / cluster scales as f32
+    bits), across families, tails and refinement rounds; plus rows that are
+    all zero, constant and with one outlier."""
+    rng = np.random.default_rng(fam * 100 + gs + rounds)
+    rows, cols = 12, gs * 3
+    w = (rng.standard_normal((rows, cols)) * 0.02).astype(np.float32)
+    w[2, 5] = 3.0
+    w[0] = 0.0
+    if fam != 2:  # 2.06 rejects a constant row (next test)
+        w[1] = 0.5
+    want = oracle.RefModel.quantize(w, fam, gs, rounds, threads=1).sections()
+    got = ccq.quantize(w, fam, gs, rounds)
+    _sections_equal(got, want)
+    # and the GPU decode of the GPU-quantized model equals the reference reconstruction
+    d = ccq.DeviceModel.upload(got)
+    assert np.array_equal(ccq.dequantize(d).view(np.uint32), oracle.dequantize(want).view(np.uint32))
+
+
+def test_gpu_quantizer_layer_size(oracle, ccq, cuda):
+    """A 256 x 4096 2.06 slab (4096 groups, 65,536 searches of 32,768 leaves
+    per round) against the reference run on all host threads."""
+    rng = np.random.default_rng(3)
+    w = (rng.standard_normal((256, 4096)) * 0.02).astype(np.float32)
+    want = oracle.RefModel.quantize(w, 2, 64, 1, threads=0).sections()
+    got = ccq.quantize(w, 2, 64, 1)
+    _sections_equal(got, want)
+
+
+def test_gpu_quantizer_206_constant_row_domain_error(oracle, ccq, cuda):
+    """A constant 2.06 row quantizes to one repeated high code word, which
+    clusters to code_scale 1 at that zero point; the reference's
+    build_cluster_table then raises DomainError (coding.hpp:145-148) - so must
+    the GPU quantizer, same text."""
+    rng = np.random.default_rng(5)
+    w = (rng.standard_normal((3, 128)) * 0.02).astype(np.float32)
+    w[1] = 0.25
+    with pytest.raises(oracle.OracleError) as ref_err:
+        oracle.RefModel.quantize(w, 2, 64, 2, threads=1)
+    with pytest.raises(ccq.DomainError) as gpu_err:
+        ccq.quantize(w, 2, 64, 2)
+    assert str(ref_err.value).split("DomainError: ")[-1] in str(gpu_err.value)
