@@ -24,5 +24,10 @@ for fam in (2, 0, 1):
     ex = P.Experts.upload([P.PackedModel.from_sections(t) for t in secs])
     offs = np.array([0, 1, 1, 3, 4], np.int32)
     P.experts_matmul(ex, offs, torch.from_numpy(O.random_matrix(4, 1088, "gaussian", 9)).cuda().to(torch.bfloat16))
+    # quantizer kernels (csrc/quantize.cu)
+    wq = (np.random.default_rng(fam).standard_normal((4, 128)) * 0.02).astype(np.float32)
+    P.quantize(wq, fam, 64, 1)
+cfg = P.ENCODINGS["2.06"]
+P.search_codes(torch.randn(40, 4, device="cuda"), torch.rand(40, dtype=torch.float64, device="cuda"), cfg, valid=3)
 torch.cuda.synchronize()
 print("sanitize case ok")
