@@ -24,6 +24,53 @@
 namespace ccqb {
 namespace {
 
+// Scan of this lane's leaves, ascending code order, strict <.  2.06 full
+// words (L=6, S=3, 4 windows) take a nested walk with prefix sums, as the
+// reference's depth-first descent: one add per leaf instead of three, and
+// the inner two levels read the same table entry on every lane (their state
+// depends only on fresh bits) - a broadcast.  The sums keep the reference's
+// left-to-right order, so costs are bitwise the same.
+__device__ __forceinline__ void leaf_scan(const double* t, int valid, int L, int S, int lane, double& best,
+                                          uint32_t& bcode) {
+  const int nst = 1 << L;
+  if (L == 6 && S == 3 && valid == 4) {
+    for (uint32_t s0 = lane; s0 < 64; s0 += 32) {
+      const double a0 = t[s0];
+      for (uint32_t f1 = 0; f1 < 8; ++f1) {
+        const uint32_t s1 = ((s0 << 3) | f1) & 63u;
+        const double a1 = __dadd_rn(a0, t[64 + s1]);
+        for (uint32_t f2 = 0; f2 < 8; ++f2) {
+          const uint32_t s2 = ((s1 << 3) | f2) & 63u;
+          const double a2 = __dadd_rn(a1, t[128 + s2]);
+#pragma unroll
+          for (uint32_t f3 = 0; f3 < 8; ++f3) {
+            const double c = __dadd_rn(a2, t[192 + (((s2 << 3) | f3) & 63u)]);
+            if (c < best) {
+              best = c;
+              bcode = (s0 << 9) | (f1 << 6) | (f2 << 3) | f3;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  const uint32_t smask = uint32_t(nst - 1), fmask = (1u << S) - 1u;
+  const uint32_t nleaf = 1u << (L + (valid - 1) * S);
+  for (uint32_t leaf = lane; leaf < nleaf; leaf += 32) {
+    uint32_t st = leaf >> ((valid - 1) * S);
+    double acc = t[st];
+    for (int j = 1; j < valid; ++j) {
+      st = ((st << S) | ((leaf >> ((valid - 1 - j) * S)) & fmask)) & smask;
+      acc = __dadd_rn(acc, t[j * nst + st]);
+    }
+    if (acc < best) {
+      best = acc;
+      bcode = leaf;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) search_codes_kernel(const float* __restrict__ targets, int64_t n,
                                                            int valid, int stride, const double* __restrict__ scales,
                                                            int zp, int L, int N, int S,
@@ -45,19 +92,7 @@ __global__ void __launch_bounds__(256) search_codes_kernel(const float* __restri
     __syncwarp();
     double best = __longlong_as_double(0x7FF0000000000000LL);  // +inf
     uint32_t bcode = 0;
-    for (uint32_t leaf = lane; leaf < nleaf; leaf += 32) {
-      uint32_t st = leaf >> ((valid - 1) * S);
-      double acc = t[st];
-      for (int j = 1; j < valid; ++j) {
-        const uint32_t f = (leaf >> ((valid - 1 - j) * S)) & fmask;
-        st = ((st << S) | f) & smask;
-        acc = __dadd_rn(acc, t[j * nst + st]);
-      }
-      if (acc < best) {
-        best = acc;
-        bcode = leaf;
-      }
-    }
+    leaf_scan(t, valid, L, S, lane, best, bcode);
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, off);
@@ -98,22 +133,9 @@ __device__ uint32_t warp_search(const float* tgt, int valid, double scale, int z
     tab[e] = __dmul_rn(d, d);
   }
   __syncwarp();
-  const uint32_t smask = uint32_t(nst - 1), fmask = (1u << S) - 1u;
-  const uint32_t nleaf = 1u << (L + (valid - 1) * S);
   double best = __longlong_as_double(0x7FF0000000000000LL);
   uint32_t bcode = 0;
-  for (uint32_t leaf = lane; leaf < nleaf; leaf += 32) {
-    uint32_t st = leaf >> ((valid - 1) * S);
-    double acc = tab[st];
-    for (int j = 1; j < valid; ++j) {
-      st = ((st << S) | ((leaf >> ((valid - 1 - j) * S)) & fmask)) & smask;
-      acc = __dadd_rn(acc, tab[j * nst + st]);
-    }
-    if (acc < best) {
-      best = acc;
-      bcode = leaf;
-    }
-  }
+  leaf_scan(tab, valid, L, S, lane, best, bcode);
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
     const double ob = __shfl_xor_sync(0xffffffffu, best, off);
