@@ -367,6 +367,9 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
     return CCQ_OK;
   }
   if (!w || !code_payload || !super_scales) return fail(CCQ_ERR_INVALID, "null pointer");
+  if (!geo.embedded_scale && !scale_payload) return fail(CCQ_ERR_INVALID, "null scale payload");
+  if (fc.cluster && (!cluster_scales || !cluster_zero_points))
+    return fail(CCQ_ERR_INVALID, "null cluster scale / zero-point output");
 
   int prev = 0;
   cudaGetDevice(&prev);
@@ -479,7 +482,6 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
     }
   }
   if (!geo.embedded_scale) {
-    if (!scale_payload) return fail(CCQ_ERR_INVALID, "null scale payload");
     std::memset(scale_payload, 0, size_t((groups + 1) / 2));
     for (int64_t gi = 0; gi < groups; ++gi) scale_payload[gi / 2] |= uint8_t(scode[size_t(gi)] << (4 * (gi % 2)));
   }
