@@ -666,6 +666,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (FAM == kF206)
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
                      : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + (((kb0 + kbs) % kChunk) / 8) * 4)));
+      // two groups in flight per warp for 2.75 / 2.5 (more ILP for their
+      // shift/mask decoders: 2-4 % at M <= 64); 2.06 is issue-bound, unchanged
+      // (profiles/r01_gemm_unroll2_experiment.txt)
+#pragma unroll(FAM == kF206 ? 1 : 2)
       for (int gg = 0; gg < ng; ++gg) {
       const int j = (kbs & 7) + gg;
       uint32_t h[32];
