@@ -234,6 +234,8 @@ bool gemv_mma_supported(const ccq_dev_model* m, int64_t M);
 // smallest batch routed to the tensor-pipe GEMV (env CCQ_FORCE_MMA=1 -> 1, for tests)
 int mma_min_tokens();
 bool gemv_mma_fits(const ccq_dev_model* m, int64_t M);
+int launch_grouped_stream(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev, int nhit,
+                          const void* x, int x_dtype, void* y, int y_dtype, cudaStream_t s);
 int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev,
                         const int32_t* offsets_host, int64_t T, const void* x, int x_dtype, void* y,
                         int y_dtype, cudaStream_t s);

@@ -35,6 +35,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "ccq_internal.hpp"
 #include "ptx.cuh"
 
@@ -160,6 +162,13 @@ struct GemvArgs {
   int64_t x_stride, y_stride;  // elements between token rows
   int streams;                 // row streams per CTA (warps = nch * streams)
   int rows_per_cta_max;
+  // grouped experts, one token per hit expert (offsets != nullptr): the model
+  // stacks E experts of rows_e rows; CTA b serves hit expert b % nhit (rows
+  // split over the CTAs of that expert), reading x row offsets[e] and
+  // writing y row offsets[e] (expert-major, y_stride = rows_e).
+  const int32_t* offsets;
+  int E;
+  int64_t rows_e;
 };
 
 __device__ __forceinline__ float load_x(const void* x, int dtype, int64_t i) {
@@ -416,10 +425,45 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int nch = L.nch;
   const int c = warp % nch;
-  const int64_t rows = L.rows, gpr = L.gpr;
-  const int64_t r_begin = int64_t(blockIdx.x) * rows / gridDim.x;
-  const int64_t r_end = int64_t(blockIdx.x + 1) * rows / gridDim.x;
+  const int64_t gpr = L.gpr;
+  int64_t r_begin, r_end, row_base = 0, tok = 0;
+  if (a.offsets) {
+    // hit experts in expert order (E <= 512): ballot compaction; the offsets
+    // are written before this launch by the host or an earlier kernel
+    __shared__ int hit[512];
+    __shared__ int wcount[16], nhit_s;
+    griddep_wait();
+    for (int e0 = 0; e0 < a.E; e0 += blockDim.x) {
+      const int e = e0 + threadIdx.x;
+      const bool has = e < a.E && a.offsets[e + 1] > a.offsets[e];
+      const unsigned bal = __ballot_sync(0xffffffffu, has);
+      if (lane == 0) wcount[warp] = __popc(bal);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = e0 == 0 ? 0 : nhit_s;
+        for (int w = 0; w < nwarps; ++w) { const int t = wcount[w]; wcount[w] = acc; acc += t; }
+        nhit_s = acc;
+      }
+      __syncthreads();
+      if (has) hit[wcount[warp] + __popc(bal & ((1u << lane) - 1u))] = e;
+      __syncthreads();
+    }
+    const int nhit = nhit_s;
+    const int h = int(blockIdx.x) % nhit, local = int(blockIdx.x) / nhit;
+    const int cnt = (int(gridDim.x) - h + nhit - 1) / nhit;
+    const int e = hit[h];
+    row_base = int64_t(e) * a.rows_e;
+    tok = a.offsets[e];
+    r_begin = row_base + int64_t(local) * a.rows_e / cnt;
+    r_end = row_base + int64_t(local + 1) * a.rows_e / cnt;
+  } else {
+    r_begin = int64_t(blockIdx.x) * L.rows / gridDim.x;
+    r_end = int64_t(blockIdx.x + 1) * L.rows / gridDim.x;
+  }
   const int nrows = int(r_end - r_begin);
+  const void* xin = a.x_dtype == CCQ_DTYPE_F32
+                        ? static_cast<const void*>(static_cast<const float*>(a.x) + tok * a.x_stride)
+                        : static_cast<const void*>(static_cast<const uint16_t*>(a.x) + tok * a.x_stride);
 
   float* part = reinterpret_cast<float*>(smem);
   float* xs = part + ((a.rows_per_cta_max * nch * MT + 31) & ~31);
@@ -492,10 +536,10 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
       float v[4];
       const int64_t e0 = int64_t(gg) * 64 + i0;
       if constexpr (XDT == CCQ_DTYPE_F32) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + e0));
+        const float4 t = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(xin) + e0));
         v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
       } else {
-        const uint2 t = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(a.x) + e0));
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(xin) + e0));
         const uint32_t hw[4] = {t.x & 0xFFFFu, t.x >> 16, t.y & 0xFFFFu, t.y >> 16};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -545,7 +589,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr * 64; e += blockDim.x) {
       const int m = int(e / (gpr * 64));
       const int64_t k = e - int64_t(m) * gpr * 64;
-      const float v = m < a.M ? load_x(a.x, a.x_dtype, int64_t(m) * a.x_stride + k) : 0.f;
+      const float v = m < a.M ? load_x(xin, a.x_dtype, int64_t(m) * a.x_stride + k) : 0.f;
       xs[m * xstride + (k >> 6) * T::XG + T::perm(int(k & 63))] = v;
     }
     __syncthreads();
@@ -649,10 +693,11 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     for (int cc = 0; cc < nch; ++cc) v += part[(rl * nch + cc) * MT + m];
     const int64_t row = r_begin + rl;
     v *= L.super[row];
+    const int64_t yi = (tok + m) * a.y_stride + (row - row_base);
     if (a.y_dtype == CCQ_DTYPE_F32)
-      static_cast<float*>(a.y)[int64_t(m) * a.y_stride + row] = v;
+      static_cast<float*>(a.y)[yi] = v;
     else
-      static_cast<__nv_bfloat16*>(a.y)[int64_t(m) * a.y_stride + row] = __float2bfloat16_rn(v);
+      static_cast<__nv_bfloat16*>(a.y)[yi] = __float2bfloat16_rn(v);
   }
   TRACE(4);
 }
@@ -723,7 +768,8 @@ __global__ void __launch_bounds__(256) gemv_generic(GenericArgs a) {
 
 template <int FAM, int RPW, int MT, int S, int XDT>
 int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
-                  void* y, int y_dtype, cudaStream_t s) {
+                  void* y, int y_dtype, cudaStream_t s, const int32_t* offsets = nullptr, int E = 0,
+                  int64_t rows_e = 0, int nhit = 0) {
   using T = G64<FAM>;
   constexpr int CGB = (32 * T::PB + 15) & ~15;
   constexpr int SB = RPW * (CGB + (FAM == kF206 ? 32 : 0));
@@ -745,8 +791,21 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   const int sms = num_sms(dev);
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const int64_t grid = std::min<int64_t>(sms, m->rows);
+  max_smem -= 2304;  // static shared memory (grouped hit list)
+  int64_t grid = std::min<int64_t>(sms, m->rows);
   a.rows_per_cta_max = int((m->rows + grid - 1) / grid);
+  if (offsets) {  // grouped: >= 1 CTA per hit expert, tokens in place
+    if (nhit < 1 || nhit > sms || E > 512) return 1;  // caller falls back
+    a.offsets = offsets;
+    a.E = E;
+    a.rows_e = rows_e;
+    a.x = x;
+    a.y = y;
+    a.M = 1;
+    a.y_stride = rows_e;
+    grid = sms;
+    a.rows_per_cta_max = int((rows_e + (grid / nhit) - 1) / (grid / nhit));
+  }
   const size_t xbytes = size_t(MT) * m->gpr * T::XG * 4 + (MT == 1 ? size_t((m->gpr + 31) & ~int64_t(31)) * 4 : 0);
   const size_t pbytes = size_t((a.rows_per_cta_max * m->nch * MT + 31) & ~31) * 4;
   const size_t xraw = 0;
@@ -851,6 +910,30 @@ bool gemv_fast_supported(const ccq_dev_model* m, int64_t M) {
   // fit one launch) or to the tcgen05 GEMM (profiles/r01_sweep.json)
   if (m->geo.group_size != 64 || m->nch > 16) return false;
   return M <= 1;
+}
+
+// Grouped experts with ONE token per hit expert on the streaming kernel
+// (returns 1 when not applicable: the caller tries the next path).
+int launch_grouped_stream(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev,
+                          int nhit, const void* x, int x_dtype, void* y, int y_dtype, cudaStream_t s) {
+  if (!offsets_dev || st->geo.group_size != 64 || st->nch > 16 || rows_e % 16 != 0) return 1;
+  if (std::getenv("CCQ_NO_GROUPED_STREAM")) return 1;
+  auto go = [&](auto fam_tag) -> int {
+    constexpr int FAM = decltype(fam_tag)::value;
+    switch (x_dtype) {
+      case CCQ_DTYPE_F32:
+        return launch_stream_dt<FAM, 4, 1, 3, CCQ_DTYPE_F32>(st, x, x_dtype, 0, 1, y, y_dtype, s, offsets_dev, E, rows_e, nhit);
+      case CCQ_DTYPE_BF16:
+        return launch_stream_dt<FAM, 4, 1, 3, CCQ_DTYPE_BF16>(st, x, x_dtype, 0, 1, y, y_dtype, s, offsets_dev, E, rows_e, nhit);
+      default:
+        return launch_stream_dt<FAM, 4, 1, 3, CCQ_DTYPE_F16>(st, x, x_dtype, 0, 1, y, y_dtype, s, offsets_dev, E, rows_e, nhit);
+    }
+  };
+  switch (st->family) {
+    case kF275: return go(std::integral_constant<int, kF275>{});
+    case kF25: return go(std::integral_constant<int, kF25>{});
+    default: return go(std::integral_constant<int, kF206>{});
+  }
 }
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,

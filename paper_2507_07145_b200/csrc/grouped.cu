@@ -111,6 +111,12 @@ extern "C" int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t
   }
   const int64_t T = offsets_host[E];
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (max_tokens == 1) {  // one token per routed expert: the CUDA-core streaming GEMV, one launch
+    int nhit = 0;
+    for (int e = 0; e < E; ++e) nhit += offsets_host[e + 1] > offsets_host[e];
+    const int st = launch_grouped_stream(stack, E, re, offsets_device, nhit, x, x_dtype, y, y_dtype, s);
+    if (st != 1) return st;
+  }
   {  // decode batches: one tensor-pipe GEMV launch over the routed experts' tiles
     const int st = launch_grouped_gemv(stack, E, re, offsets_device, offsets_host, T, x, x_dtype, y, y_dtype, s);
     if (st != 1) return st;

@@ -383,6 +383,7 @@ def test_experts_decode_grouped_gemv(oracle, ccq, cuda, counts, xdt, fam, path, 
     tokens are skipped.  2.06 on the record kernel and on the TMA-box kernel
     (CCQ_NO_REC), 2.75 / 2.5 on the TMA-box kernel."""
     torch = cuda
+    monkeypatch.setenv("CCQ_NO_GROUPED_STREAM", "1")  # one-token batches would take the streaming kernel
     if path == "box":
         monkeypatch.setenv("CCQ_NO_REC", "1")
     E, rows, cols = 8, 48, 1024 + 64
@@ -649,3 +650,31 @@ def test_k_heavy_206_small_batch_on_gemm(oracle, ccq, cuda, M):
     for r0, r1 in ((0, 16), (4080, 4096)):
         want = oracle.gemv_batch(_slice_rows(oracle, s, r0, r1), x, threads=8)
         assert rel_err(y[:, r0:r1].cpu().numpy(), want) < REL_TOL
+
+
+@pytest.mark.parametrize("fam", [2, 0, 1])
+@pytest.mark.parametrize("E,hits,rows,cols", [(8, [0, 1, 3, 4, 7], 48, 1024 + 64), (8, list(range(8)), 64, 4096),
+                                              (64, [3, 9, 17, 20, 33, 40, 51, 63], 48, 2048),
+                                              (160, list(range(0, 160)), 16, 512)])
+@pytest.mark.parametrize("xdt", ["bf16", "f32"])
+def test_experts_one_token_per_expert_streaming(oracle, ccq, cuda, fam, E, hits, rows, cols, xdt):
+    """MoE decode with one token per routed expert runs the CUDA-core
+    streaming GEMV in grouped mode (gemv.cu: CTA b serves hit expert
+    b % nhit, x / y rows at the expert's offset); 160 hit experts exceed the
+    SM count and take the tensor-pipe path instead."""
+    torch = cuda
+    counts = [1 if e in hits else 0 for e in range(E)]
+    secs, offs, x, want = _expert_case(oracle, fam, E, rows, cols, counts, seed=E + rows + fam)
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s_) for s_ in secs])
+    if xdt == "bf16":
+        xt = torch.from_numpy(bf16_round(x)).cuda().to(torch.bfloat16)
+        for e in range(E):
+            if counts[e]:
+                want[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], bf16_round(x[offs[e]:offs[e + 1]]), threads=8)
+    else:
+        xt = torch.from_numpy(x).cuda()
+    y = ccq.experts_matmul(ex, offs, xt)
+    torch.cuda.synchronize()
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
+    yb = ccq.experts_matmul(ex, offs, xt, out_dtype=torch.bfloat16)
+    assert rel_err(yb.float().cpu().numpy(), want) < 4e-3
