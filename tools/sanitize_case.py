@@ -24,6 +24,8 @@ for fam in (2, 0, 1):
     ex = P.Experts.upload([P.PackedModel.from_sections(t) for t in secs])
     offs = np.array([0, 1, 1, 3, 4], np.int32)
     P.experts_matmul(ex, offs, torch.from_numpy(O.random_matrix(4, 1088, "gaussian", 9)).cuda().to(torch.bfloat16))
+    offs1 = np.array([0, 1, 1, 2, 3], np.int32)  # one token per routed expert: grouped streaming GEMV
+    P.experts_matmul(ex, offs1, torch.from_numpy(O.random_matrix(3, 1088, "gaussian", 10)).cuda().to(torch.bfloat16))
     # quantizer kernels (csrc/quantize.cu)
     wq = (np.random.default_rng(fam).standard_normal((4, 128)) * 0.02).astype(np.float32)
     P.quantize(wq, fam, 64, 1)
