@@ -293,6 +293,103 @@ __global__ void cluster_research(const float* __restrict__ W, int64_t rows, int6
   }
 }
 
+
+// quantize_scales (packing.cpp:142-158), one warp per row: super scale, the
+// snapped scale codes and group_scales = float(code) * super.  A negative or
+// NaN raw scale flags the row (the reference's DomainError).
+__global__ void snap_scales(const float* __restrict__ raw, int64_t rows, int64_t gpr, uint32_t levels,
+                            float* __restrict__ super, uint16_t* __restrict__ scode, float* __restrict__ gscale,
+                            unsigned long long* __restrict__ bad_row) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const float* rs = raw + r * gpr;
+    float mx = 0.0f;
+    bool bad = false;
+    for (int64_t j = lane; j < gpr; j += 32) {
+      const float v = rs[j];
+      bad |= v < 0.0f || isnan(v);
+      mx = fmaxf(mx, v);  // max of non-negative floats: order-free
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) atomicMin(bad_row, (unsigned long long)r);
+      continue;
+    }
+    const float sup = mx == 0.0f ? 1.0f : float(__ddiv_rn(double(mx), double(levels)));
+    if (lane == 0) super[r] = sup;
+    for (int64_t j = lane; j < gpr; j += 32) {
+      long c = lround(__ddiv_rn(double(rs[j]), double(sup)));
+      c = c < 0 ? 0 : (c > long(levels) ? long(levels) : c);
+      scode[r * gpr + j] = uint16_t(c);
+      gscale[r * gpr + j] = __fmul_rn(float(c), sup);
+    }
+  }
+}
+
+// cluster_channel + build_cluster_table (quantizer.cpp:224-270), one warp per
+// row: code range -> (code_scale, code_zero_point), the 256 widened codes and
+// their states; a code outside [0, 2^code_bits) flags (row, q).
+__global__ void cluster_tables(const uint16_t* __restrict__ words, int64_t rows, int64_t wpr, QScheme q,
+                               float* __restrict__ cscale, float* __restrict__ czp, uint8_t* __restrict__ tstates,
+                               uint16_t* __restrict__ tcodes, unsigned long long* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    uint32_t lo = 0xFFFFu, hi = 0u;
+    for (int64_t i = lane; i < wpr; i += 32) {
+      const uint32_t v = words[r * wpr + i];
+      lo = v < lo ? v : lo;
+      hi = v > hi ? v : hi;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+    }
+    const float zp = float(lo);
+    const float cs = hi == lo ? 1.0f : float(__ddiv_rn(double(hi) - double(lo), 255.0));
+    if (lane == 0) {
+      cscale[r] = cs;
+      czp[r] = zp;
+    }
+    for (int c = lane; c < 256; c += 32) {
+      const long v = lround(__dadd_rn(__dmul_rn(double(c), double(cs)), double(zp)));
+      if (v < 0 || v >= (1l << q.code_bits)) {
+        atomicMin(bad, (unsigned long long)(r * 256 + c));
+        continue;
+      }
+      tcodes[r * 256 + c] = uint16_t(v);
+      for (int j = 0; j < q.wpw; ++j) tstates[(r * 256 + c) * 8 + j] = uint8_t((uint32_t(v) >> q.shifts[j]) & q.wmask);
+    }
+  }
+}
+
+// pack_model's payload (container.cpp:323-358, pack_group packing.cpp:71-114):
+// one thread per group; words little-endian, the tail word of embedded-scale
+// families carries the scale code.  Side-band nibbles: one thread per byte.
+__global__ void pack_groups(const uint16_t* __restrict__ words, const uint8_t* __restrict__ clustered,
+                            const uint16_t* __restrict__ scode, int64_t groups, QScheme q, int word_bytes,
+                            int embedded, uint8_t* __restrict__ payload, uint8_t* __restrict__ nibbles) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t gi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+    uint8_t* out = payload + gi * q.words * word_bytes;
+    for (int w = 0; w < q.words; ++w) {
+      uint32_t v = clustered ? clustered[gi * q.words + w] : words[gi * q.words + w];
+      if (q.has_tail && w == q.full_words && !clustered) v |= scode[gi];
+      out[w * word_bytes] = uint8_t(v & 0xFF);
+      if (word_bytes == 2) out[w * word_bytes + 1] = uint8_t(v >> 8);
+    }
+  }
+  if (!embedded)
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < (groups + 1) / 2; b += stride) {
+      uint32_t v = scode[2 * b] & 0xFu;
+      if (2 * b + 1 < groups) v |= (scode[2 * b + 1] & 0xFu) << 4;
+      nibbles[b] = uint8_t(v);
+    }
+}
+
 }  // namespace
 }  // namespace ccqb
 
@@ -331,12 +428,10 @@ extern "C" int ccq_cuda_search_codes(const float* targets, int64_t n, int32_t va
 }
 
 // ---- quantize_tensor + pack_model on the GPU (host driver) -----------------
-// Per-group search and refinement (quantize_groups) and the 2.06 cluster
-// re-search (cluster_research) run on the device; the per-row O(groups)
-// steps - scale snapping (quantize_scales, packing.cpp:142-158), the code
-// cluster range (cluster_channel, quantizer.cpp:224-247), the 256-entry
-// cluster tables (build_cluster_table, 258-270) and byte packing
-// (pack_group / pack_cluster_scales, packing.cpp:71-114, 160-170) - on the host.
+// Everything runs on the device, one stream-ordered chain and one sync: the
+// per-group search and refinement (quantize_groups), scale snapping
+// (snap_scales), the 2.06 code clusters and tables (cluster_tables) and
+// cluster-aware re-search (cluster_research), and byte packing (pack_groups).
 extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size,
                                  int32_t rounds, int32_t device, uint8_t* code_payload, uint8_t* scale_payload,
                                  float* super_scales, float* cluster_scales, float* cluster_zero_points) {
@@ -374,116 +469,69 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
   int prev = 0;
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
-  float *dW = nullptr, *draw = nullptr, *dgs = nullptr;
-  uint16_t *dwords = nullptr, *dtcodes = nullptr;
-  uint8_t *dts = nullptr, *dcl = nullptr;
-  std::vector<uint16_t> words(size_t(nw), 0);
-  std::vector<float> raw(static_cast<size_t>(groups));
-  std::vector<uint16_t> scode(static_cast<size_t>(groups));
-  std::vector<float> gscale(static_cast<size_t>(groups));
-  std::vector<uint8_t> clustered(fc.cluster ? size_t(nw) : 0);
-  auto cleanup = [&] {
-    cudaFree(dW); cudaFree(draw); cudaFree(dgs); cudaFree(dwords); cudaFree(dtcodes); cudaFree(dts); cudaFree(dcl);
-    cudaSetDevice(prev);
-  };
-  if (e == cudaSuccess) e = cudaMalloc(&dW, size_t(rows * cols) * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&draw, size_t(groups) * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&dwords, size_t(nw) * 2);
-  if (e == cudaSuccess) e = cudaMemcpy(dW, w, size_t(rows * cols) * 4, cudaMemcpyHostToDevice);
+  // device workspace (one allocation): W | words | raw | scode | gscale |
+  // super | cs | czp | tables | clustered | payload | nibbles | flags
+  const uint32_t levels = (1u << fc.scale_bits) - 1u;
+  const size_t pay = size_t(groups) * size_t(geo.payload_bytes), nib = geo.embedded_scale ? 0 : size_t((groups + 1) / 2);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off = (off + bytes + 255) & ~size_t(255); return o; };
+  const size_t oW = take(size_t(rows * cols) * 4), oWd = take(size_t(nw) * 2), oRaw = take(size_t(groups) * 4);
+  const size_t oSc = take(size_t(groups) * 2), oGs = take(size_t(groups) * 4), oSup = take(size_t(rows) * 4);
+  const size_t oCs = take(fc.cluster ? size_t(rows) * 4 : 0), oCz = take(fc.cluster ? size_t(rows) * 4 : 0);
+  const size_t oTs = take(fc.cluster ? size_t(rows) * 256 * 8 : 0), oTc = take(fc.cluster ? size_t(rows) * 256 * 2 : 0);
+  const size_t oCl = take(fc.cluster ? size_t(nw) : 0), oPay = take(pay), oNib = take(nib), oFlag = take(16);
+  uint8_t* ws = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&ws, off);
+  auto P8 = [&](size_t o) { return ws + o; };
+  unsigned long long flags[2] = {~0ull, ~0ull};  // [0] bad scale row, [1] bad cluster (row * 256 + q)
+  if (e == cudaSuccess) e = cudaMemcpy(P8(oW), w, size_t(rows * cols) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P8(oFlag), flags, sizeof(flags), cudaMemcpyHostToDevice);
+  const float* dW = reinterpret_cast<const float*>(P8(oW));
+  uint16_t* dwords = reinterpret_cast<uint16_t*>(P8(oWd));
+  uint16_t* dscode = reinterpret_cast<uint16_t*>(P8(oSc));
+  float* dgs = reinterpret_cast<float*>(P8(oGs));
+  unsigned long long* dflag = reinterpret_cast<unsigned long long*>(P8(oFlag));
+  const int sms = num_sms(device);
   if (e == cudaSuccess) {
-    const int64_t blocks = std::min<int64_t>((groups + kQWarps - 1) / kQWarps, int64_t(num_sms(device)) * 8);
-    quantize_groups<<<unsigned(blocks), kQWarps * 32>>>(dW, rows, cols, q, rounds, dwords, draw);
+    const int64_t blocks = std::min<int64_t>((groups + kQWarps - 1) / kQWarps, int64_t(sms) * 8);
+    quantize_groups<<<unsigned(blocks), kQWarps * 32>>>(dW, rows, cols, q, rounds, dwords,
+                                                       reinterpret_cast<float*>(P8(oRaw)));
+    const unsigned rb = unsigned(std::min<int64_t>((rows + 7) / 8, int64_t(sms) * 16));
+    snap_scales<<<rb, 256>>>(reinterpret_cast<const float*>(P8(oRaw)), rows, gpr, levels,
+                             reinterpret_cast<float*>(P8(oSup)), dscode, dgs, dflag);
+    count_launch(2);
+    if (fc.cluster) {
+      cluster_tables<<<rb, 256>>>(dwords, rows, gpr * q.words, q, reinterpret_cast<float*>(P8(oCs)),
+                                  reinterpret_cast<float*>(P8(oCz)), P8(oTs), reinterpret_cast<uint16_t*>(P8(oTc)),
+                                  dflag + 1);
+      const int64_t cb = std::min<int64_t>((nw + 255) / 256, int64_t(sms) * 16);
+      cluster_research<<<unsigned(cb), 256>>>(dW, rows, cols, q, dgs, P8(oTs), reinterpret_cast<uint16_t*>(P8(oTc)),
+                                              P8(oCl), dwords);
+      count_launch(2);
+    }
+    const int64_t pb = std::min<int64_t>((groups + 255) / 256, int64_t(sms) * 16);
+    pack_groups<<<unsigned(pb), 256>>>(dwords, fc.cluster ? P8(oCl) : nullptr, dscode, groups, q, fc.word_bytes,
+                                       geo.embedded_scale, P8(oPay), P8(oNib));
     count_launch();
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = cudaMemcpy(words.data(), dwords, size_t(nw) * 2, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess) e = cudaMemcpy(raw.data(), draw, size_t(groups) * 4, cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) {
-    cleanup();
-    return cuda_fail(e, "gpu quantizer");
+  if (e == cudaSuccess) e = cudaMemcpy(flags, P8(oFlag), sizeof(flags), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && flags[0] == ~0ull && flags[1] == ~0ull) {
+    e = cudaMemcpy(code_payload, P8(oPay), pay, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && nib) e = cudaMemcpy(scale_payload, P8(oNib), nib, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(super_scales, P8(oSup), size_t(rows) * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && fc.cluster) e = cudaMemcpy(cluster_scales, P8(oCs), size_t(rows) * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && fc.cluster)
+      e = cudaMemcpy(cluster_zero_points, P8(oCz), size_t(rows) * 4, cudaMemcpyDeviceToHost);
   }
-  // quantize_scales per row (packing.cpp:142-158)
-  const uint32_t levels = (1u << fc.scale_bits) - 1u;
-  for (int64_t r = 0; r < rows; ++r) {
-    float mx = 0.0f;
-    for (int64_t j = 0; j < gpr; ++j) {
-      const float sv = raw[size_t(r * gpr + j)];
-      if (sv < 0.0f || std::isnan(sv)) {
-        cleanup();
-        return fail(CCQ_ERR_DOMAIN, "group scales must be non-negative");
-      }
-      mx = std::max(mx, sv);
-    }
-    const float sup = mx == 0.0f ? 1.0f : float(double(mx) / double(levels));
-    super_scales[r] = sup;
-    for (int64_t j = 0; j < gpr; ++j) {
-      const long c = std::lround(double(raw[size_t(r * gpr + j)]) / double(sup));
-      const uint16_t code = uint16_t(std::clamp<long>(c, 0, long(levels)));
-      scode[size_t(r * gpr + j)] = code;
-      gscale[size_t(r * gpr + j)] = float(code) * sup;
-    }
-  }
-  if (fc.cluster) {
-    // cluster_channel + build_cluster_table per row, re-search on the device
-    std::vector<uint8_t> tstates(size_t(rows) * 256 * 8, 0);
-    std::vector<uint16_t> tcodes(size_t(rows) * 256);
-    for (int64_t r = 0; r < rows; ++r) {
-      const uint16_t* rw = words.data() + size_t(r * gpr * q.words);
-      uint16_t lo = rw[0], hi = rw[0];
-      for (int64_t i = 0; i < gpr * q.words; ++i) {
-        lo = std::min(lo, rw[i]);
-        hi = std::max(hi, rw[i]);
-      }
-      const float czp = float(lo);
-      const float cs = hi == lo ? 1.0f : float((double(hi) - double(lo)) / 255.0);
-      cluster_scales[r] = cs;
-      cluster_zero_points[r] = czp;
-      for (int c = 0; c < 256; ++c) {
-        const long v = std::lround(double(c) * double(cs) + double(czp));
-        if (v < 0 || v >= (1l << fc.code_bits)) {
-          cleanup();
-          return fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^" + std::to_string(fc.code_bits) +
-                                          "): q=" + std::to_string(c));
-        }
-        tcodes[size_t(r * 256 + c)] = uint16_t(v);
-        for (int j = 0; j < fc.wpw; ++j)
-          tstates[size_t((r * 256 + c) * 8 + j)] = uint8_t((uint32_t(v) >> fc.shifts[j]) & fc.weight_mask);
-      }
-    }
-    e = cudaMalloc(&dgs, size_t(groups) * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&dts, tstates.size());
-    if (e == cudaSuccess) e = cudaMalloc(&dtcodes, tcodes.size() * 2);
-    if (e == cudaSuccess) e = cudaMalloc(&dcl, size_t(nw));
-    if (e == cudaSuccess) e = cudaMemcpy(dgs, gscale.data(), size_t(groups) * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(dts, tstates.data(), tstates.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(dtcodes, tcodes.data(), tcodes.size() * 2, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) {
-      const int64_t blocks = std::min<int64_t>((nw + 255) / 256, int64_t(num_sms(device)) * 16);
-      cluster_research<<<unsigned(blocks), 256>>>(dW, rows, cols, q, dgs, dts, dtcodes, dcl, dwords);
-      count_launch();
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaMemcpy(clustered.data(), dcl, size_t(nw), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) {
-      cleanup();
-      return cuda_fail(e, "gpu quantizer (cluster re-search)");
-    }
-  }
-  cleanup();
-  // pack_model (container.cpp:323-358): payload words little-endian, tail
-  // word carries the scale code (embedded families), side-band nibbles.
-  uint8_t* out = code_payload;
-  for (int64_t gi = 0; gi < groups; ++gi) {
-    for (int wd = 0; wd < q.words; ++wd) {
-      uint32_t v = fc.cluster ? clustered[size_t(gi * q.words + wd)] : words[size_t(gi * q.words + wd)];
-      if (geo.has_tail && wd == q.full_words && !fc.cluster) v |= scode[size_t(gi)];
-      *out++ = uint8_t(v & 0xFF);
-      if (fc.word_bytes == 2) *out++ = uint8_t(v >> 8);
-    }
-  }
-  if (!geo.embedded_scale) {
-    std::memset(scale_payload, 0, size_t((groups + 1) / 2));
-    for (int64_t gi = 0; gi < groups; ++gi) scale_payload[gi / 2] |= uint8_t(scode[size_t(gi)] << (4 * (gi % 2)));
-  }
+  cudaFree(ws);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "gpu quantizer");
+  // errors in row order: a row's scales are snapped before it is clustered
+  if (flags[0] != ~0ull && (flags[1] == ~0ull || flags[0] <= flags[1] / 256))
+    return fail(CCQ_ERR_DOMAIN, "group scales must be non-negative");
+  if (flags[1] != ~0ull)
+    return fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^" + std::to_string(fc.code_bits) +
+                                    "): q=" + std::to_string(int(flags[1] % 256)));
   return CCQ_OK;
 }
