@@ -7,6 +7,7 @@
 #include <string>
 
 #include "ccq/container.hpp"
+#include "ccq/tensor.hpp"
 #include "ccq_cuda.h"
 
 namespace ccq::cuda {
@@ -38,6 +39,13 @@ class DeviceModel {
   explicit DeviceModel(ccq_dev_model* h) : h_(h) {}
   ccq_dev_model* h_ = nullptr;
 };
+
+// pack_model(quantize_tensor(weights, {family, group_size, rounds})) with the
+// search, refinement, scale snapping, clustering and packing on `device`
+// (quantizer.cpp:319-425, container.cpp:323-358); the sections are
+// bit-identical to the reference's.  group_size <= 256.
+PackedModel quantize(const Matrix& weights, Family family, int group_size = 64, int rounds = 2,
+                     int device = 0);
 
 }  // namespace ccq::cuda
 

@@ -210,6 +210,31 @@ void DeviceModel::matmul(const void* x, DType xd, std::int64_t M, void* y, DType
   throw_status(ccq_cuda_matmul(h_, x, int(xd), M, y, int(yd), stream));
 }
 
+PackedModel quantize(const Matrix& weights, Family family, int group_size, int rounds, int device) {
+  std::int32_t g[6];
+  throw_status(ccq_group_geometry(std::int32_t(family), group_size, g));
+  PackedModel m;
+  m.rows = weights.rows;
+  m.cols = weights.cols;
+  m.family = family;
+  m.group_size = group_size;
+  m.rounds = rounds;
+  const std::int64_t groups = group_size > 0 ? weights.rows * (weights.cols / group_size) : 0;
+  m.code_payload.resize(std::size_t(groups) * std::size_t(g[5]));
+  if (!g[4]) m.scale_payload.resize(std::size_t((groups + 1) / 2));
+  m.super_scales.resize(std::size_t(weights.rows));
+  if (family == Family::Bpw206) {
+    m.cluster_scales.resize(std::size_t(weights.rows));
+    m.cluster_zero_points.resize(std::size_t(weights.rows));
+  }
+  throw_status(ccq_quantize_host(weights.data.data(), weights.rows, weights.cols, std::int32_t(family), group_size,
+                                 rounds, device, m.code_payload.data(),
+                                 m.scale_payload.empty() ? nullptr : m.scale_payload.data(), m.super_scales.data(),
+                                 m.cluster_scales.empty() ? nullptr : m.cluster_scales.data(),
+                                 m.cluster_zero_points.empty() ? nullptr : m.cluster_zero_points.data()));
+  return m;
+}
+
 }  // namespace cuda
 
 }  // namespace ccq

@@ -126,3 +126,26 @@ def test_gpu_quantizer_206_constant_row_domain_error(oracle, ccq, cuda):
     with pytest.raises(ccq.DomainError) as gpu_err:
         ccq.quantize(w, 2, 64, 2)
     assert str(ref_err.value).split("DomainError: ")[-1] in str(gpu_err.value)
+
+
+@pytest.mark.parametrize("name,fam", [("2.06", 2), ("2.75", 0), ("2.5", 1)])
+def test_cpp_api_quantize_matches_reference(oracle, ccq, cuda, tmp_path, name, fam):
+    """The drop-in C++ API (ccq::cuda::quantize, tools/ccq_gpu_quantize.cpp)
+    writes the reference quantizer's sections byte for byte."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    lib_dir = os.path.join(ROOT, "paper_2507_07145_b200")
+    exe = tmp_path / "ccq_gpu_quantize"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(ROOT, "tools", "ccq_gpu_quantize.cpp"), "-o", str(exe),
+                    os.path.join(lib_dir, "libccq_b200.so"), f"-Wl,-rpath,{lib_dir}"], check=True)
+    w = (np.random.default_rng(fam).standard_normal((16, 256)) * 0.02).astype(np.float32)
+    src, dst = tmp_path / "w.f32", tmp_path / "out.bin"
+    w.tofile(src)
+    r = subprocess.run([str(exe), str(src), "16", "256", name, "64", "2", str(dst)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    s = oracle.RefModel.quantize(w, fam, 64, 2, threads=1).sections()
+    want = b"".join(np.ascontiguousarray(a).tobytes() for a in
+                    (s.code_payload, s.scale_payload, s.super_scales, s.cluster_scales, s.cluster_zero_points))
+    assert dst.read_bytes() == want
