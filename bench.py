@@ -462,7 +462,7 @@ def run_moe(P, torch, dev, stream, hbm_peak, tflops_peak):
         ex = P.Experts.upload(models, device=dev.index)
         del models
         rng = np.random.default_rng(7)
-        for B in (1, 16, 64, 256, 4096):  # decode batches and a 4096-token prefill
+        for B in (1, 2, 4, 16, 64, 256, 4096):  # decode batches and a 4096-token prefill
             counts = np.zeros(E, np.int64)
             for _ in range(B):
                 counts[rng.choice(E, 8, replace=False)] += 1

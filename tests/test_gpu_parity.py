@@ -678,3 +678,27 @@ def test_experts_one_token_per_expert_streaming(oracle, ccq, cuda, fam, E, hits,
     assert rel_err(y.cpu().numpy(), want) < REL_TOL
     yb = ccq.experts_matmul(ex, offs, xt, out_dtype=torch.bfloat16)
     assert rel_err(yb.float().cpu().numpy(), want) < 4e-3
+
+
+@pytest.mark.parametrize("fam", [2, 0, 1])
+@pytest.mark.parametrize("counts,rows,cols", [([2, 0, 1, 2, 0, 0, 1, 2], 48, 1024 + 64), ([2] * 8, 64, 4096),
+                                              ([0, 2, 0, 0, 1, 0, 2, 0] * 8, 32, 2048)])
+@pytest.mark.parametrize("xdt", ["bf16", "f32"])
+def test_experts_two_tokens_per_expert(oracle, ccq, cuda, fam, counts, rows, cols, xdt):
+    """Up to two tokens per routed expert (mixed 0 / 1 / 2): routed to the
+    grouped tensor-pipe GEMV (a grouped M = 2 streaming variant measured 5x
+    slower, profiles/r01_moe_grouped_stream_m2_experiment.txt)."""
+    torch = cuda
+    E = len(counts)
+    secs, offs, x, want = _expert_case(oracle, fam, E, rows, cols, counts, seed=E * 7 + rows + fam)
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s_) for s_ in secs])
+    if xdt == "bf16":
+        xt = torch.from_numpy(bf16_round(x)).cuda().to(torch.bfloat16)
+        for e in range(E):
+            if counts[e]:
+                want[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], bf16_round(x[offs[e]:offs[e + 1]]), threads=8)
+    else:
+        xt = torch.from_numpy(x).cuda()
+    y = ccq.experts_matmul(ex, offs, xt)
+    torch.cuda.synchronize()
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
