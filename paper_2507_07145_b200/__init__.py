@@ -354,9 +354,15 @@ def _stream_ptr(stream):
     return C.c_void_p(getattr(stream, "cuda_stream", stream))
 
 
+_DTYPE_CODES = None
+
+
 def _torch_dtype_code(t) -> int:
-    import torch
-    return {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}[t.dtype]
+    global _DTYPE_CODES
+    if _DTYPE_CODES is None:
+        import torch
+        _DTYPE_CODES = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+    return _DTYPE_CODES[t.dtype]
 
 
 def decode(model: DeviceModel, levels=None, weights=None, stream=None) -> None:
@@ -378,8 +384,8 @@ def matmul(model: DeviceModel, x, out=None, kernel: str = "auto", out_dtype=None
     if out is None:
         out = torch.empty(x.shape[0], model.rows, dtype=out_dtype or torch.float32,
                           device=x.device)
-    fn = {"auto": lib().ccq_cuda_matmul, "gemv": lib().ccq_cuda_gemv,
-          "gemm": lib().ccq_cuda_gemm}[kernel]
+    L = lib()
+    fn = L.ccq_cuda_matmul if kernel == "auto" else {"gemv": L.ccq_cuda_gemv, "gemm": L.ccq_cuda_gemm}[kernel]
     _check(fn(model.h, x.data_ptr(), _torch_dtype_code(x), x.shape[0], out.data_ptr(),
               _torch_dtype_code(out), _stream_ptr(stream)))
     return out

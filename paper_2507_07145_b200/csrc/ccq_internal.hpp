@@ -242,6 +242,7 @@ int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const in
 int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                     int y_dtype, cudaStream_t s);
 int num_sms(int device);
+int max_smem_optin(int device);  // cached cudaDevAttrMaxSharedMemoryPerBlockOptin
 // Library-owned stream-ordered memory pool of `device` (release threshold =
 // unlimited, so per-call scratch does not re-map memory after every sync).
 cudaMemPool_t scratch_pool(int device);

@@ -789,8 +789,7 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = num_sms(dev);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int max_smem = max_smem_optin(dev);
   max_smem -= 2304;  // static shared memory (grouped hit list)
   int64_t grid = std::min<int64_t>(sms, m->rows);
   a.rows_per_cta_max = int((m->rows + grid - 1) / grid);
@@ -891,6 +890,17 @@ int launch_generic(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
 }
 
 }  // namespace
+
+int max_smem_optin(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) device = 0;
+  if (!cached[device]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cached[device] = v > 0 ? v : 232448;
+  }
+  return cached[device];
+}
 
 int num_sms(int device) {
   static int cached[64] = {0};

@@ -1079,8 +1079,7 @@ int launch_fam_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int max_smem = max_smem_optin(dev);
   const int ntiles = int((m->rows + kRowsT - 1) / kRowsT);
   const int grid = std::min(num_sms(dev), ntiles);
   const size_t xb = x_dtype == CCQ_DTYPE_F32 ? 4 : 2, yb = y_dtype == CCQ_DTYPE_F32 ? 4 : 2;
@@ -1119,8 +1118,7 @@ bool gemv_mma_fits(const ccq_dev_model* m, int64_t M) {
   if (M < 1 || M > 8 || !gemv_mma_supported(m, M)) return false;
   int dev = 0;
   cudaGetDevice(&dev);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int max_smem = max_smem_optin(dev);
   const int ntiles = int((m->rows + 15) / 16);
   const int grid = std::min(num_sms(dev), ntiles);
   Cfg cfg{};
@@ -1152,8 +1150,7 @@ int launch_grouped_box(const ccq_dev_model* st, int E, int64_t rows_e, const int
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int max_smem = max_smem_optin(dev);
   const int grid = std::min(num_sms(dev), ntiles);
   const Cfg cfg = wmax > 8 ? plan_cfg<FAM, 2, S>(st, wmax, grid, max_smem, ntiles)
                            : plan_cfg<FAM, 1, S>(st, wmax, grid, max_smem, ntiles);
@@ -1186,8 +1183,7 @@ int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const in
   const int ntiles = nhit * tpe;
   int dev = 0;
   cudaGetDevice(&dev);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int max_smem = max_smem_optin(dev);
   const int grid = std::min(num_sms(dev), ntiles);
   // the largest token window any CTA stages (same partition as the kernel)
   std::vector<int> hits;
@@ -1245,8 +1241,7 @@ int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
       if (m->plan_pos_min >= 1 && M <= 16 && m->rec == uint32_t(m->cgb + 32) && !std::getenv("CCQ_NO_REC")) {
         int dev = 0;
         cudaGetDevice(&dev);
-        int max_smem = 0;
-        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        int max_smem = max_smem_optin(dev);
         const int grid = std::min<int>(num_sms(dev), int((m->rows + kRowsT - 1) / kRowsT));
         const RecCfg rc = rec_cfg(m, int(M), grid, max_smem);
         if (rc.S > 0) {
