@@ -10,6 +10,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2507_07145_b200 as P  # noqa: E402
+
+if os.environ.get("CCQ_LIB"):  # experiment builds (tools only)
+    P.LIB_PATH = os.path.join(os.path.dirname(P.__file__), os.environ["CCQ_LIB"])
 from paper_2507_07145_b200.synthetic import random_packed  # noqa: E402
 
 ap = argparse.ArgumentParser()
