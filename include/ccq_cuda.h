@@ -225,6 +225,13 @@ int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int32_t family
                       int32_t rounds, int32_t device, uint8_t* code_payload, uint8_t* scale_payload,
                       float* super_scales, float* cluster_scales, float* cluster_zero_points);
 
+/* Quantize weights already in device memory (w: rows x cols f32, device
+ * pointer) and upload the result as a device model, with no host round trip
+ * (the packed sections go from the quantizer's workspace into the device
+ * re-layout).  Same sections as ccq_quantize_host. */
+int ccq_cuda_quantize_model(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size,
+                            int32_t rounds, int32_t device, ccq_dev_model** out);
+
 #ifdef __cplusplus
 }
 #endif

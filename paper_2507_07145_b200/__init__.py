@@ -32,7 +32,7 @@ __all__ = [
     "CcqError", "ConfigError", "DomainError", "ShapeError", "EncodingError", "FormatError",
     "CudaError", "FAMILIES", "PackedModel", "DeviceModel", "load_model", "dequantize", "gemv",
     "gemv_batch", "model_payload_bytes", "group_geometry", "clustered_code_value", "decode",
-    "matmul", "grouped", "search_codes", "quantize", "ENCODINGS", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
+    "matmul", "grouped", "search_codes", "quantize", "quantize_to_device", "ENCODINGS", "lib", "LIB_PATH", "launch_count", "Experts", "experts_matmul",
     "moe_forward",
 ]
 
@@ -103,7 +103,7 @@ ABI_SYMBOLS = [
     "ccq_gemv_host", "ccq_gemv_batch_host", "ccq_model_payload_bytes", "ccq_group_geometry",
     "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
     "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward", "ccq_cuda_search_codes",
-    "ccq_quantize_host",
+    "ccq_quantize_host", "ccq_cuda_quantize_model",
 ]
 
 _lib = None
@@ -139,6 +139,7 @@ def lib():
         L.ccq_cuda_moe_forward.argtypes = [vp, vp, vp, i64, i32, vp, C.c_int, vp, C.c_int, vp]
         L.ccq_cuda_search_codes.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i32, vp, vp]
         L.ccq_quantize_host.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        L.ccq_cuda_quantize_model.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp]
         L.ccq_dequantize_host.argtypes = [vp, vp]
         L.ccq_gemv_host.argtypes = [vp, vp, u64, vp, u64]
         L.ccq_gemv_batch_host.argtypes = [vp, vp, i64, i64, vp, i64, i64]
@@ -498,6 +499,22 @@ def quantize(weights, family, group_size: int = 64, rounds: int = 2, device: int
     _check(lib().ccq_quantize_host(_np_ptr(w), rows, cols, fam, group_size, rounds, device, _np_ptr(code),
                                    _np_ptr(scale), _np_ptr(sup), _np_ptr(cs), _np_ptr(czp)))
     return PackedModel(rows, cols, fam, group_size, code, scale, sup, cs, czp, rounds)
+
+
+def quantize_to_device(weights, family, group_size: int = 64, rounds: int = 2) -> DeviceModel:
+    """Weights already on the GPU (torch f32 CUDA tensor [rows, cols]) ->
+    quantized, packed and uploaded DeviceModel, no host round trip
+    (ccq_cuda_quantize_model)."""
+    if weights.dim() != 2 or not weights.is_cuda or not weights.is_contiguous():
+        raise ShapeError("weights must be a contiguous 2-D CUDA tensor")
+    import torch
+    if weights.dtype != torch.float32:
+        raise ShapeError("weights must be float32")
+    fam = FAMILIES[family] if isinstance(family, str) else int(family)
+    h = C.c_void_p()
+    _check(lib().ccq_cuda_quantize_model(weights.data_ptr(), weights.shape[0], weights.shape[1], fam, group_size,
+                                         rounds, weights.device.index or 0, C.byref(h)))
+    return DeviceModel(h)
 
 
 def grouped(models, offsets, x, out=None, out_dtype=None, stream=None):

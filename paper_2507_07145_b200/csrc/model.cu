@@ -325,7 +325,8 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
   // Staging: the row range's code bytes and nibbles exactly as stored, the
-  // cluster parameters, invalid-q masks and two result words.
+  // cluster parameters, invalid-q masks and two result words.  The view's
+  // sections may be host or device memory (cudaMemcpyDefault, UVA).
   const uint64_t code_len = uint64_t(rows) * row_bytes;
   const uint64_t nib_lo = geo.embedded_scale ? 0 : (uint64_t(r0) * gpr) / 2;
   const uint64_t nib_hi = geo.embedded_scale ? 0 : (uint64_t(r1) * gpr + 1) / 2;
@@ -343,17 +344,17 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   }
   if (e == cudaSuccess) e = cudaMemset(m->base, 0, total);
   if (e == cudaSuccess && code_len)
-    e = cudaMemcpy(stage, v->code_payload + uint64_t(r0) * row_bytes, code_len, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(stage, v->code_payload + uint64_t(r0) * row_bytes, code_len, cudaMemcpyDefault);
   if (e == cudaSuccess && nib_hi > nib_lo)
-    e = cudaMemcpy(stage + s_nib, v->scale_payload + nib_lo, nib_hi - nib_lo, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(stage + s_nib, v->scale_payload + nib_lo, nib_hi - nib_lo, cudaMemcpyDefault);
   if (e == cudaSuccess && rows)
     e = cudaMemcpy(static_cast<uint8_t*>(m->base) + off_super, v->super_scales + r0, size_t(rows) * 4,
-                   cudaMemcpyHostToDevice);
+                   cudaMemcpyDefault);
   if (e == cudaSuccess && fc.cluster && rows) {
-    e = cudaMemcpy(stage + s_ab, v->cluster_scales + r0, size_t(rows) * 4, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(stage + s_ab, v->cluster_scales + r0, size_t(rows) * 4, cudaMemcpyDefault);
     if (e == cudaSuccess)
       e = cudaMemcpy(stage + s_ab + size_t(rows) * 4, v->cluster_zero_points + r0, size_t(rows) * 4,
-                     cudaMemcpyHostToDevice);
+                     cudaMemcpyDefault);
   }
   if (e == cudaSuccess) e = cudaMemcpy(stage + s_res, res, sizeof(res), cudaMemcpyHostToDevice);
   int64_t plan_fail = rows;  // first row without an exact plan
@@ -391,7 +392,8 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   // we raise it at upload for any stored byte), or a row without an exact plan.
   const int64_t bad_row = bad == ~0ull ? rows : int64_t(bad / row_bytes);
   if (bad_row < rows && bad_row <= plan_fail) {
-    const uint8_t q = v->code_payload[uint64_t(r0) * row_bytes + bad];
+    uint8_t q = 0;  // the view may live on the host or the device
+    cudaMemcpy(&q, v->code_payload + uint64_t(r0) * row_bytes + bad, 1, cudaMemcpyDefault);
     cudaFree(m->base);
     delete m;
     return fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^15): q=" + std::to_string(int(q)) +

@@ -432,11 +432,22 @@ extern "C" int ccq_cuda_search_codes(const float* targets, int64_t n, int32_t va
 // per-group search and refinement (quantize_groups), scale snapping
 // (snap_scales), the 2.06 code clusters and tables (cluster_tables) and
 // cluster-aware re-search (cluster_research), and byte packing (pack_groups).
-extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size,
-                                 int32_t rounds, int32_t device, uint8_t* code_payload, uint8_t* scale_payload,
-                                 float* super_scales, float* cluster_scales, float* cluster_zero_points) {
+namespace ccqb {
+namespace {
+
+struct QuantRun {
+  uint8_t* ws = nullptr;  // device workspace; the packed sections live in it
+  size_t oPay = 0, oNib = 0, oSup = 0, oCs = 0, oCz = 0;
+  size_t pay = 0, nib = 0;
   Geometry geo;
-  int st = geometry_for(family, group_size, &geo);  // ConfigError as group_geometry
+  FamilyConst fc;
+};
+
+// Validates like quantize_tensor, runs the device chain; on CCQ_OK the
+// sections are in r.ws (caller frees).  w is host or device memory.
+int run_quantizer(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size, int32_t rounds,
+                  int32_t device, QuantRun& r) {
+  int st = geometry_for(family, group_size, &r.geo);  // ConfigError as group_geometry
   if (st != CCQ_OK) return st;
   if (rounds < 0) return fail(CCQ_ERR_CONFIG, "refinement rounds must be >= 0");
   if (rows < 0 || cols < 0) return fail(CCQ_ERR_SHAPE, "negative shape");
@@ -444,7 +455,9 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
     return fail(CCQ_ERR_SHAPE, "input dimension " + std::to_string(cols) + " is not a multiple of group size " +
                                    std::to_string(group_size));
   if (group_size > kQMaxGS) return fail(CCQ_ERR_CONFIG, "the GPU quantizer takes group sizes up to 256");
+  const Geometry& geo = r.geo;
   const FamilyConst fc = family_const(family);
+  r.fc = fc;
   QScheme q{};
   if (family == kF275) {
     q.nparts = 1; q.L[0] = 4; q.N[0] = 3; q.S[0] = 2;
@@ -457,14 +470,7 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
   q.full_words = geo.full_words; q.has_tail = geo.has_tail; q.words = geo.words_per_group; q.wmask = fc.weight_mask;
   for (int i = 0; i < 8; ++i) q.shifts[i] = i < 7 ? fc.shifts[i] : 0;
   const int64_t gpr = cols / group_size, groups = rows * gpr, nw = groups * q.words;
-  if (groups == 0) {
-    for (int64_t r = 0; r < rows; ++r) super_scales[r] = 1.0f;
-    return CCQ_OK;
-  }
-  if (!w || !code_payload || !super_scales) return fail(CCQ_ERR_INVALID, "null pointer");
-  if (!geo.embedded_scale && !scale_payload) return fail(CCQ_ERR_INVALID, "null scale payload");
-  if (fc.cluster && (!cluster_scales || !cluster_zero_points))
-    return fail(CCQ_ERR_INVALID, "null cluster scale / zero-point output");
+  if (!w && groups) return fail(CCQ_ERR_INVALID, "null weights");
 
   int prev = 0;
   cudaGetDevice(&prev);
@@ -472,19 +478,26 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
   // device workspace (one allocation): W | words | raw | scode | gscale |
   // super | cs | czp | tables | clustered | payload | nibbles | flags
   const uint32_t levels = (1u << fc.scale_bits) - 1u;
-  const size_t pay = size_t(groups) * size_t(geo.payload_bytes), nib = geo.embedded_scale ? 0 : size_t((groups + 1) / 2);
+  r.pay = size_t(groups) * size_t(geo.payload_bytes);
+  r.nib = geo.embedded_scale ? 0 : size_t((groups + 1) / 2);
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t o = off; off = (off + bytes + 255) & ~size_t(255); return o; };
   const size_t oW = take(size_t(rows * cols) * 4), oWd = take(size_t(nw) * 2), oRaw = take(size_t(groups) * 4);
-  const size_t oSc = take(size_t(groups) * 2), oGs = take(size_t(groups) * 4), oSup = take(size_t(rows) * 4);
-  const size_t oCs = take(fc.cluster ? size_t(rows) * 4 : 0), oCz = take(fc.cluster ? size_t(rows) * 4 : 0);
+  const size_t oSc = take(size_t(groups) * 2), oGs = take(size_t(groups) * 4);
+  r.oSup = take(size_t(rows) * 4);
+  r.oCs = take(fc.cluster ? size_t(rows) * 4 : 0);
+  r.oCz = take(fc.cluster ? size_t(rows) * 4 : 0);
   const size_t oTs = take(fc.cluster ? size_t(rows) * 256 * 8 : 0), oTc = take(fc.cluster ? size_t(rows) * 256 * 2 : 0);
-  const size_t oCl = take(fc.cluster ? size_t(nw) : 0), oPay = take(pay), oNib = take(nib), oFlag = take(16);
+  const size_t oCl = take(fc.cluster ? size_t(nw) : 0);
+  r.oPay = take(r.pay);
+  r.oNib = take(r.nib);
+  const size_t oFlag = take(16);
   uint8_t* ws = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&ws, off);
+  r.ws = ws;
   auto P8 = [&](size_t o) { return ws + o; };
   unsigned long long flags[2] = {~0ull, ~0ull};  // [0] bad scale row, [1] bad cluster (row * 256 + q)
-  if (e == cudaSuccess) e = cudaMemcpy(P8(oW), w, size_t(rows * cols) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && groups) e = cudaMemcpy(P8(oW), w, size_t(rows * cols) * 4, cudaMemcpyDefault);
   if (e == cudaSuccess) e = cudaMemcpy(P8(oFlag), flags, sizeof(flags), cudaMemcpyHostToDevice);
   const float* dW = reinterpret_cast<const float*>(P8(oW));
   uint16_t* dwords = reinterpret_cast<uint16_t*>(P8(oWd));
@@ -492,17 +505,20 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
   float* dgs = reinterpret_cast<float*>(P8(oGs));
   unsigned long long* dflag = reinterpret_cast<unsigned long long*>(P8(oFlag));
   const int sms = num_sms(device);
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && groups == 0) {  // no groups: super scales are 1 (quantize_scales of nothing)
+    std::vector<float> ones(size_t(rows), 1.0f);
+    if (rows) e = cudaMemcpy(P8(r.oSup), ones.data(), size_t(rows) * 4, cudaMemcpyHostToDevice);
+  } else if (e == cudaSuccess) {
     const int64_t blocks = std::min<int64_t>((groups + kQWarps - 1) / kQWarps, int64_t(sms) * 8);
     quantize_groups<<<unsigned(blocks), kQWarps * 32>>>(dW, rows, cols, q, rounds, dwords,
                                                        reinterpret_cast<float*>(P8(oRaw)));
     const unsigned rb = unsigned(std::min<int64_t>((rows + 7) / 8, int64_t(sms) * 16));
     snap_scales<<<rb, 256>>>(reinterpret_cast<const float*>(P8(oRaw)), rows, gpr, levels,
-                             reinterpret_cast<float*>(P8(oSup)), dscode, dgs, dflag);
+                             reinterpret_cast<float*>(P8(r.oSup)), dscode, dgs, dflag);
     count_launch(2);
     if (fc.cluster) {
-      cluster_tables<<<rb, 256>>>(dwords, rows, gpr * q.words, q, reinterpret_cast<float*>(P8(oCs)),
-                                  reinterpret_cast<float*>(P8(oCz)), P8(oTs), reinterpret_cast<uint16_t*>(P8(oTc)),
+      cluster_tables<<<rb, 256>>>(dwords, rows, gpr * q.words, q, reinterpret_cast<float*>(P8(r.oCs)),
+                                  reinterpret_cast<float*>(P8(r.oCz)), P8(oTs), reinterpret_cast<uint16_t*>(P8(oTc)),
                                   dflag + 1);
       const int64_t cb = std::min<int64_t>((nw + 255) / 256, int64_t(sms) * 16);
       cluster_research<<<unsigned(cb), 256>>>(dW, rows, cols, q, dgs, P8(oTs), reinterpret_cast<uint16_t*>(P8(oTc)),
@@ -511,27 +527,97 @@ extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int
     }
     const int64_t pb = std::min<int64_t>((groups + 255) / 256, int64_t(sms) * 16);
     pack_groups<<<unsigned(pb), 256>>>(dwords, fc.cluster ? P8(oCl) : nullptr, dscode, groups, q, fc.word_bytes,
-                                       geo.embedded_scale, P8(oPay), P8(oNib));
+                                       geo.embedded_scale, P8(r.oPay), P8(r.oNib));
     count_launch();
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(flags, P8(oFlag), sizeof(flags), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && flags[0] == ~0ull && flags[1] == ~0ull) {
-    e = cudaMemcpy(code_payload, P8(oPay), pay, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess && nib) e = cudaMemcpy(scale_payload, P8(oNib), nib, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess) e = cudaMemcpy(super_scales, P8(oSup), size_t(rows) * 4, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess && fc.cluster) e = cudaMemcpy(cluster_scales, P8(oCs), size_t(rows) * 4, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess && fc.cluster)
-      e = cudaMemcpy(cluster_zero_points, P8(oCz), size_t(rows) * 4, cudaMemcpyDeviceToHost);
-  }
-  cudaFree(ws);
   cudaSetDevice(prev);
-  if (e != cudaSuccess) return cuda_fail(e, "gpu quantizer");
+  if (e != cudaSuccess) {
+    cudaFree(ws);
+    r.ws = nullptr;
+    return cuda_fail(e, "gpu quantizer");
+  }
   // errors in row order: a row's scales are snapped before it is clustered
+  int bad = CCQ_OK;
   if (flags[0] != ~0ull && (flags[1] == ~0ull || flags[0] <= flags[1] / 256))
-    return fail(CCQ_ERR_DOMAIN, "group scales must be non-negative");
-  if (flags[1] != ~0ull)
-    return fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^" + std::to_string(fc.code_bits) +
-                                    "): q=" + std::to_string(int(flags[1] % 256)));
-  return CCQ_OK;
+    bad = fail(CCQ_ERR_DOMAIN, "group scales must be non-negative");
+  else if (flags[1] != ~0ull)
+    bad = fail(CCQ_ERR_DOMAIN, "clustered code reconstructs outside [0, 2^" + std::to_string(fc.code_bits) +
+                                   "): q=" + std::to_string(int(flags[1] % 256)));
+  if (bad != CCQ_OK) {
+    cudaFree(ws);
+    r.ws = nullptr;
+  }
+  return bad;
+}
+
+}  // namespace
+}  // namespace ccqb
+
+extern "C" int ccq_quantize_host(const float* w, int64_t rows, int64_t cols, int32_t family, int32_t group_size,
+                                 int32_t rounds, int32_t device, uint8_t* code_payload, uint8_t* scale_payload,
+                                 float* super_scales, float* cluster_scales, float* cluster_zero_points) {
+  Geometry g0;
+  if (geometry_for(family, group_size, &g0) == CCQ_OK) {  // output pointer checks before any work
+    const bool cl = family_const(family).cluster;
+    if ((rows && !super_scales) || (!g0.embedded_scale && rows && cols && !scale_payload) ||
+        (rows && cols && !code_payload) || (cl && rows && (!cluster_scales || !cluster_zero_points)))
+      return fail(CCQ_ERR_INVALID, "null output section");
+  }
+  QuantRun r;
+  const int st = run_quantizer(w, rows, cols, family, group_size, rounds, device, r);
+  if (st != CCQ_OK) return st;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t e = cudaSuccess;
+  if (r.pay) e = cudaMemcpy(code_payload, r.ws + r.oPay, r.pay, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && r.nib) e = cudaMemcpy(scale_payload, r.ws + r.oNib, r.nib, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && rows) e = cudaMemcpy(super_scales, r.ws + r.oSup, size_t(rows) * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && r.fc.cluster && rows) {
+    e = cudaMemcpy(cluster_scales, r.ws + r.oCs, size_t(rows) * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(cluster_zero_points, r.ws + r.oCz, size_t(rows) * 4, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(r.ws);
+  cudaSetDevice(prev);
+  return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gpu quantizer copy-out");
+}
+
+// Quantize weights already in HBM and upload the result as a device model,
+// with no host round trip: the packed sections go from the quantizer's
+// workspace straight into the device re-layout (ccq_cuda_model_upload takes
+// device-resident views).
+extern "C" int ccq_cuda_quantize_model(const float* w, int64_t rows, int64_t cols, int32_t family,
+                                       int32_t group_size, int32_t rounds, int32_t device, ccq_dev_model** out) {
+  if (!out) return fail(CCQ_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  QuantRun r;
+  const int st = run_quantizer(w, rows, cols, family, group_size, rounds, device, r);
+  if (st != CCQ_OK) return st;
+  ccq_packed_view v{};
+  v.rows = rows;
+  v.cols = cols;
+  v.family = family;
+  v.group_size = group_size;
+  v.rounds = rounds;
+  v.code_payload = r.ws + r.oPay;
+  v.code_bytes = r.pay;
+  v.scale_payload = r.nib ? r.ws + r.oNib : nullptr;
+  v.scale_bytes = r.nib;
+  v.super_scales = reinterpret_cast<const float*>(r.ws + r.oSup);
+  v.n_super_scales = uint64_t(rows);
+  if (r.fc.cluster) {
+    v.cluster_scales = reinterpret_cast<const float*>(r.ws + r.oCs);
+    v.n_cluster_scales = uint64_t(rows);
+    v.cluster_zero_points = reinterpret_cast<const float*>(r.ws + r.oCz);
+    v.n_cluster_zero_points = uint64_t(rows);
+  }
+  const int up = ccq_cuda_model_upload(&v, device, out);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaFree(r.ws);
+  cudaSetDevice(prev);
+  return up;
 }
