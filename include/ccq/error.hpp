@@ -32,7 +32,8 @@ class EncodingError : public Error {
 class FormatError : public Error {
  public:
   explicit FormatError(const std::string& what, long long offset = -1)
-      : Error(what), offset_(offset) {}
+      : Error(offset >= 0 ? what + " (byte offset " + std::to_string(offset) + ")" : what),
+        offset_(offset) {}
   long long offset() const { return offset_; }
 
  private:

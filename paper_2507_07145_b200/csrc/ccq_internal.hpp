@@ -185,6 +185,20 @@ inline DevLayout layout_of(const ccq_dev_model* m) {
                    m->cgb, m->rec, m->nch, m->geo};
 }
 
+// Makes `d` the current device for the scope of a call (device-pointer entry
+// points run on the model's device whatever the caller's current device is).
+struct DeviceScope {
+  int prev = 0;
+  bool changed = false;
+  explicit DeviceScope(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) changed = cudaSetDevice(d) == cudaSuccess;
+  }
+  ~DeviceScope() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
 // Thread-local error message + status helpers.
 void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
@@ -242,6 +256,10 @@ int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const in
 int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                     int y_dtype, cudaStream_t s);
 int num_sms(int device);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `kern` on the CURRENT
+// device, once per (kernel, device) and only when `bytes` grows; thread-safe
+// (the attribute is per device, the library may drive several GPUs).
+int ensure_smem(const void* kern, size_t bytes);
 int max_smem_optin(int device);  // cached cudaDevAttrMaxSharedMemoryPerBlockOptin
 // Library-owned stream-ordered memory pool of `device` (release threshold =
 // unlimited, so per-call scratch does not re-map memory after every sync).

@@ -3,11 +3,14 @@
 // container.hpp:37-83, coding.hpp:115-150, packing.hpp:38-49 of the reference.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <sstream>
 #include <cstring>
-#include <map>
+#include <list>
+#include <memory>
 #include <mutex>
-#include <tuple>
 
 #include "ccq/coding.hpp"
 #include "ccq/container.hpp"
@@ -33,34 +36,6 @@ void throw_status(int st) {
   }
 }
 
-std::string family_name(Family family) {
-  switch (family) {
-    case Family::Bpw275: return "2.75";
-    case Family::Bpw25: return "2.5";
-    case Family::Bpw206: return "2.06";
-  }
-  throw ConfigError("unknown family");
-}
-
-Family family_from_name(const std::string& name) {
-  if (name == "2.75") return Family::Bpw275;
-  if (name == "2.5" || name == "2.50") return Family::Bpw25;
-  if (name == "2.06") return Family::Bpw206;
-  throw ConfigError("unknown family '" + name + "' (expected 2.75, 2.5 or 2.06)");
-}
-
-std::uint16_t clustered_code_value(std::uint8_t q, float a, float b, int code_bits) {
-  std::uint16_t out = 0;
-  throw_status(ccq_clustered_code_value(q, a, b, code_bits, &out));
-  return out;
-}
-
-GroupGeometry group_geometry(Family family, int group_size) {
-  int32_t g[6];
-  throw_status(ccq_group_geometry(int32_t(family), group_size, g));
-  return GroupGeometry{g[0], g[1], g[2] != 0, g[3], g[4] != 0, g[5]};
-}
-
 namespace {
 
 ccq_packed_view view_of(const PackedModel& m) {
@@ -83,28 +58,94 @@ ccq_packed_view view_of(const PackedModel& m) {
   return v;
 }
 
-// Upload cache for the synchronous reference-signature calls.  PackedModel
-// is immutable after load by contract; the key also covers the
-// section pointers and sizes so a reallocated model re-uploads.
-using Key = std::tuple<const PackedModel*, const void*, size_t, const void*, size_t, const void*,
-                       int64_t, int64_t, int, int, int>;
+// Upload cache for the synchronous reference-signature calls.  The reference
+// reads the PackedModel on every call (kernels.cpp:103-187), so a cached
+// device copy may only be reused when the sections are byte-identical: the
+// key is a 64-bit content hash over every section plus the shape, family,
+// group size and device - never the object's address (a freed model's
+// addresses are reused by the next same-shape model).  Entries are shared
+// (a concurrent eviction cannot free a copy still in use) and the cache is
+// bounded by bytes (LRU), so device memory is returned.
+struct Entry {
+  std::uint64_t hash;
+  std::int64_t rows, cols;
+  int family, group_size, device;
+  std::shared_ptr<ccq_dev_model> model;
+  std::uint64_t bytes;
+};
 std::mutex g_mu;
-std::map<Key, ccq_dev_model*> g_cache;
+std::list<Entry> g_cache;  // most recently used first
+std::uint64_t g_cache_bytes = 0;
+constexpr std::uint64_t kCacheBytes = 4ull << 30;
 
-const ccq_dev_model* device_copy(const PackedModel& m) {
+// Four independent multiply-rotate lanes over 8-byte words (memory-bound on
+// the host); the tail and the section lengths are folded in so sections of
+// different sizes never collide by construction of the stream.
+std::uint64_t hash_bytes(const void* p, std::size_t n, std::uint64_t seed) {
+  constexpr std::uint64_t k1 = 0x9E3779B185EBCA87ull, k2 = 0xC2B2AE3D27D4EB4Full;
+  auto rotl = [](std::uint64_t v, int r) { return (v << r) | (v >> (64 - r)); };
+  const auto* b = static_cast<const unsigned char*>(p);
+  std::uint64_t h[4] = {seed ^ k1, seed ^ k2, seed + k1, seed - k2};
+  auto block = [&](const unsigned char* q) {
+    for (int l = 0; l < 4; ++l) {
+      std::uint64_t v;
+      std::memcpy(&v, q + 8 * l, 8);
+      h[l] = rotl(h[l] + v * k2, 31) * k1;
+    }
+  };
+  std::size_t i = 0;
+  for (; i + 32 <= n; i += 32) block(b + i);
+  if (i < n) {  // zero-padded tail block; the length below disambiguates it
+    unsigned char tail[32] = {};
+    std::memcpy(tail, b + i, n - i);
+    block(tail);
+  }
+  std::uint64_t r = rotl(h[0], 1) + rotl(h[1], 7) + rotl(h[2], 12) + rotl(h[3], 18);
+  r ^= std::uint64_t(n) * k1;
+  r ^= r >> 33;
+  r *= k2;
+  r ^= r >> 29;
+  return r;
+}
+
+std::uint64_t content_hash(const PackedModel& m) {
+  std::uint64_t h = 0x243F6A8885A308D3ull;
+  h = hash_bytes(m.code_payload.data(), m.code_payload.size(), h);
+  h = hash_bytes(m.scale_payload.data(), m.scale_payload.size(), h);
+  h = hash_bytes(m.super_scales.data(), m.super_scales.size() * 4, h);
+  h = hash_bytes(m.cluster_scales.data(), m.cluster_scales.size() * 4, h);
+  h = hash_bytes(m.cluster_zero_points.data(), m.cluster_zero_points.size() * 4, h);
+  return h;
+}
+
+std::shared_ptr<const ccq_dev_model> device_copy(const PackedModel& m) {
   int dev = 0;
   cudaGetDevice(&dev);
-  Key k{&m, m.code_payload.data(), m.code_payload.size(), m.scale_payload.data(),
-        m.scale_payload.size(), m.super_scales.data(), m.rows, m.cols, int(m.family),
-        m.group_size, dev};
-  std::lock_guard<std::mutex> lock(g_mu);
-  auto it = g_cache.find(k);
-  if (it != g_cache.end()) return it->second;
+  const std::uint64_t h = content_hash(m);
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+      if (it->hash == h && it->rows == m.rows && it->cols == m.cols && it->family == int(m.family) &&
+          it->group_size == m.group_size && it->device == dev) {
+        g_cache.splice(g_cache.begin(), g_cache, it);
+        return g_cache.front().model;
+      }
+    }
+  }
   const ccq_packed_view v = view_of(m);
-  ccq_dev_model* h = nullptr;
-  throw_status(ccq_cuda_model_upload(&v, dev, &h));
-  g_cache.emplace(k, h);
-  return h;
+  ccq_dev_model* raw = nullptr;
+  throw_status(ccq_cuda_model_upload(&v, dev, &raw));
+  std::shared_ptr<ccq_dev_model> sp(raw, [](ccq_dev_model* p) { ccq_cuda_model_free(p); });
+  ccq_model_info info{};
+  ccq_cuda_model_info(raw, &info);
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_cache.push_front(Entry{h, m.rows, m.cols, int(m.family), m.group_size, dev, sp, info.device_bytes});
+  g_cache_bytes += info.device_bytes;
+  while (g_cache.size() > 1 && g_cache_bytes > kCacheBytes) {
+    g_cache_bytes -= g_cache.back().bytes;
+    g_cache.pop_back();  // freed once the last caller releases it
+  }
+  return sp;
 }
 
 }  // namespace
@@ -133,20 +174,20 @@ PackedModel load_model(const std::string& path) {
 
 Matrix dequantize(const PackedModel& model) {
   Matrix out(model.rows, model.cols);
-  throw_status(ccq_dequantize_host(device_copy(model), out.data.data()));
+  throw_status(ccq_dequantize_host(device_copy(model).get(), out.data.data()));
   return out;
 }
 
 void gemv(const PackedModel& model, std::span<const float> x, std::span<float> y) {
   if (std::int64_t(x.size()) != model.cols || std::int64_t(y.size()) != model.rows)
     throw ShapeError("gemv operand sizes do not match the model shape");
-  throw_status(ccq_gemv_host(device_copy(model), x.data(), x.size(), y.data(), y.size()));
+  throw_status(ccq_gemv_host(device_copy(model).get(), x.data(), x.size(), y.data(), y.size()));
 }
 
 void gemv_batch(const PackedModel& model, const Matrix& x, Matrix& y) {
   if (x.cols != model.cols || y.cols != model.rows || y.rows != x.rows)
     throw ShapeError("gemv_batch operand shapes do not match the model shape");
-  throw_status(ccq_gemv_batch_host(device_copy(model), x.data.data(), x.rows, x.cols,
+  throw_status(ccq_gemv_batch_host(device_copy(model).get(), x.data.data(), x.rows, x.cols,
                                    y.data.data(), y.rows, y.cols));
 }
 
@@ -165,6 +206,138 @@ std::uint64_t model_payload_bytes(const PackedModel& model) {
   return std::uint64_t(model.code_payload.size()) + model.scale_payload.size() +
          model.super_scales.size() * 4 + model.cluster_scales.size() * 4 +
          model.cluster_zero_points.size() * 4;
+}
+
+// ---- bench report (kernels.hpp:53-76, kernels.cpp:211-300) ----
+
+namespace {
+
+double median_of(std::vector<double> v) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const std::size_t n = v.size();
+  return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+
+template <class F>
+double host_ms(F&& f) {
+  const auto t0 = std::chrono::steady_clock::now();
+  f();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+std::vector<BenchRow> bench_model(const PackedModel& model, const std::vector<int>& batches, int iterations,
+                                  std::uint64_t seed) {
+  if (iterations < 1) throw ConfigError("bench iterations must be at least 1");
+  for (int b : batches)
+    if (b < 1) throw ConfigError("bench batch size must be at least 1");
+  const Matrix dense = dequantize(model);
+  const std::uint64_t payload = model_payload_bytes(model);
+  const std::uint64_t dense_bytes = std::uint64_t(model.rows) * std::uint64_t(model.cols) * 4;
+  int dev = 0;
+  throw_status(cudaGetDevice(&dev) == cudaSuccess ? CCQ_OK : CCQ_ERR_CUDA);
+  const cuda::DeviceModel resident(model, dev);
+  std::vector<BenchRow> out;
+  for (int batch : batches) {
+    const Matrix x = random_matrix(batch, model.cols, Distribution::Gaussian, seed + std::uint64_t(batch));
+    Matrix y(batch, model.rows);
+    auto dense_product = [&](const Matrix& w) {
+      for (std::int64_t m = 0; m < batch; ++m) dense_gemv(w, x.row(m), y.row(m));
+    };
+    std::vector<double> t_dense, t_dequant, t_fused, t_gpu;
+    for (int it = 0; it < iterations; ++it) {
+      t_dense.push_back(host_ms([&] { dense_product(dense); }));
+      t_dequant.push_back(host_ms([&] { dense_product(dequantize(model)); }));
+      t_fused.push_back(host_ms([&] { gemv_batch(model, x, y); }));
+    }
+    // device-resident activations: CUDA events around the launch alone
+    {
+      void *dx = nullptr, *dy = nullptr;
+      const std::size_t xb = x.data.size() * 4, yb = y.data.size() * 4;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      cudaError_t e = cudaMalloc(&dx, xb);
+      if (e == cudaSuccess) e = cudaMalloc(&dy, yb);
+      if (e == cudaSuccess) e = cudaMemcpy(dx, x.data.data(), xb, cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaEventCreate(&e0);
+      if (e == cudaSuccess) e = cudaEventCreate(&e1);
+      for (int it = -1; e == cudaSuccess && it < iterations; ++it) {  // it = -1: warm-up
+        cudaEventRecord(e0, nullptr);
+        resident.matmul(dx, cuda::DType::F32, batch, dy, cuda::DType::F32, nullptr);
+        cudaEventRecord(e1, nullptr);
+        e = cudaEventSynchronize(e1);
+        float ms = 0.f;
+        if (e == cudaSuccess && it >= 0 && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess) t_gpu.push_back(ms);
+      }
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+      if (dx) cudaFree(dx);
+      if (dy) cudaFree(dy);
+      if (e != cudaSuccess) throw CudaError(std::string("bench_model: ") + cudaGetErrorString(e));
+    }
+    const BenchRow base{model.cols, model.rows, batch, "", 0.0, 0};
+    auto row = [&](const char* variant, const std::vector<double>& t, std::uint64_t bytes) {
+      BenchRow r = base;
+      r.variant = variant;
+      r.median_ms = median_of(t);
+      r.bytes_read = bytes;
+      out.push_back(r);
+    };
+    row("dense_f32", t_dense, dense_bytes);
+    row("dequant_then_dense", t_dequant, payload + dense_bytes);
+    row("ccq_fused", t_fused, payload);
+    row("ccq_gpu_fused", t_gpu, payload);
+  }
+  return out;
+}
+
+std::string bench_csv(const std::vector<BenchRow>& rows) {
+  std::ostringstream o;
+  o << "shape,M,variant,median_ms,bytes_read\n";
+  for (const BenchRow& r : rows)
+    o << r.d_in << 'x' << r.d_out << ',' << r.batch << ',' << r.variant << ',' << r.median_ms << ','
+      << r.bytes_read << '\n';
+  return o.str();
+}
+
+std::vector<BenchRow> parse_bench_csv(const std::string& csv) {
+  // Same acceptance as the reference reader: four comma-terminated fields
+  // then the byte count (the rest of the line); numbers parse as std::sto*.
+  std::istringstream in(csv);
+  std::string line;
+  if (!std::getline(in, line) || line != "shape,M,variant,median_ms,bytes_read")
+    throw FormatError("bench csv header mismatch", 0);
+  std::vector<BenchRow> rows;
+  while (std::getline(in, line)) {
+    if (line.empty()) continue;
+    std::string f[5];
+    std::size_t p = 0;
+    int n = 0;
+    for (; n < 4; ++n) {
+      const std::size_t c = line.find(',', p);
+      if (c == std::string::npos) break;
+      f[n] = line.substr(p, c - p);
+      p = c + 1;
+    }
+    if (n < 4 || p >= line.size()) throw FormatError("bench csv row with missing fields: " + line, 0);
+    f[4] = line.substr(p);
+    const std::size_t xpos = f[0].find('x');
+    if (xpos == std::string::npos) throw FormatError("bench csv shape not AxB: " + f[0], 0);
+    BenchRow r;
+    try {
+      r.d_in = std::stoll(f[0].substr(0, xpos));
+      r.d_out = std::stoll(f[0].substr(xpos + 1));
+      r.batch = std::stoi(f[1]);
+      r.median_ms = std::stod(f[3]);
+      r.bytes_read = std::stoull(f[4]);
+    } catch (const std::exception&) {
+      throw FormatError("bench csv row with non-numeric fields: " + line, 0);
+    }
+    r.variant = f[2];
+    rows.push_back(r);
+  }
+  return rows;
 }
 
 namespace cuda {

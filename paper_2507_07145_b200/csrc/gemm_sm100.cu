@@ -878,10 +878,9 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
              offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr};
   auto kern = gemm_ccq<FAM, BN>;
-  static bool configured[5] = {};
-  if (!configured[BN / 64]) {
-    CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL));
-    configured[BN / 64] = true;
+  if (int st2 = ensure_smem(reinterpret_cast<const void*>(kern), SM::TOTAL)) {
+    cudaFreeAsync(x16, s);
+    return st2;
   }
   const int tb = BN / xs;
   dim3 grid = grouped ? dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe))

@@ -35,7 +35,10 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "ccq_internal.hpp"
 #include "ptx.cuh"
@@ -818,12 +821,7 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   }
   if (a.streams < 1) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");
   auto kern = gemv_stream<FAM, RPW, MT, S, XDT>;
-  static size_t configured[3][5][5][3] = {};
-  size_t& conf = configured[FAM][RPW][MT][XDT];
-  if (conf < smem) {
-    CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    conf = smem;
-  }
+  if (int st = ensure_smem(reinterpret_cast<const void*>(kern), smem)) return st;
   // Programmatic stream serialization: the prologue and the weight copies of
   // this launch overlap the tail of the previous kernel in the stream (the
   // kernel waits on griddepcontrol before touching x or y).
@@ -902,6 +900,19 @@ int max_smem_optin(int device) {
   return cached[device];
 }
 
+int ensure_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  CCQ_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kern, dev}];
+  if (have >= bytes) return CCQ_OK;
+  CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  have = bytes;
+  return CCQ_OK;
+}
+
 int num_sms(int device) {
   static int cached[64] = {0};
   if (device < 0 || device >= 64) return 148;
@@ -951,7 +962,11 @@ int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
   if (x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && M >= mma_min_tokens() &&
       gemv_mma_supported(m, M))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, s);
-  const bool fast = m->geo.group_size == 64 && m->nch <= 16;
+  // the streaming kernel reads x with 16-byte (f32) / 8-byte (bf16, f16)
+  // vector loads: an unaligned view takes the scalar kernel
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+  const bool aligned = (xa & (x_dtype == CCQ_DTYPE_F32 ? 15u : 7u)) == 0;
+  const bool fast = m->geo.group_size == 64 && m->nch <= 16 && aligned;
   switch (m->family) {
     case kF275:
       return fast ? launch_fam<kF275>(m, x, x_dtype, M, y, y_dtype, s)

@@ -965,12 +965,7 @@ int launch_rec(const ccq_dev_model* m, const void* x, int M, void* y, int x_dtyp
   a.E = E;
   a.rows_e = rows_e;
   auto kern = gemv_rec206<NT, XDT, GROUPED>;
-  static size_t configured[3][3][2] = {};
-  size_t& conf = configured[NT][XDT][GROUPED ? 1 : 0];
-  if (conf < cfg.smem) {
-    CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)));
-    conf = cfg.smem;
-  }
+  if (int st = ensure_smem(reinterpret_cast<const void*>(kern), cfg.smem)) return st;
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(unsigned(grid));
   lc.blockDim = dim3(13u * 32u);
@@ -1038,12 +1033,7 @@ int launch_chunk(const ccq_dev_model* m, const CUtensorMap& tmc, const CUtensorM
   a.E = E;
   a.rows_e = rows_e;
   auto kern = gemv_mma<FAM, NT, S, XDT, P2, GROUPED>;
-  static size_t configured[3][3][2] = {};
-  size_t& conf = configured[NT][XDT][P2 ? 1 : 0];
-  if (conf < cfg.smem) {
-    CCQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cfg.smem)));
-    conf = cfg.smem;
-  }
+  if (int st = ensure_smem(reinterpret_cast<const void*>(kern), cfg.smem)) return st;
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(unsigned(grid));
   lc.blockDim = dim3(unsigned(cfg.warps * 32));

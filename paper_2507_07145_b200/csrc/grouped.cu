@@ -101,6 +101,7 @@ extern "C" int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t
                                        void* y, int y_dtype, void* stream) {
   if (!stack || !offsets_host || stack->num_experts <= 0)
     return fail(CCQ_ERR_INVALID, "not a stacked-expert model or null offsets");
+  DeviceScope ds(stack->device);
   const int E = stack->num_experts;
   const int64_t re = stack->rows_per_expert;
   int64_t max_tokens = 0;

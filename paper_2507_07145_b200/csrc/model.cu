@@ -459,6 +459,7 @@ int ccq_model_payload_bytes(const ccq_dev_model* m, uint64_t* out) {
 
 int ccq_cuda_decode(const ccq_dev_model* m, int8_t* levels, float* weights, void* stream) {
   if (!m) return fail(CCQ_ERR_INVALID, "null model");
+  DeviceScope ds(m->device);
   if (!levels && !weights) return CCQ_OK;
   return launch_decode(m, levels, weights, static_cast<cudaStream_t>(stream));
 }
@@ -476,6 +477,7 @@ int ccq_cuda_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M,
   if (M < 0) return fail(CCQ_ERR_SHAPE, "negative batch");
   int st = check_dtypes(x_dtype, y_dtype);
   if (st != CCQ_OK || M == 0 || m->rows == 0) return st;
+  DeviceScope ds(m->device);
   return launch_gemv(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
 }
 
@@ -487,6 +489,7 @@ int ccq_cuda_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M,
   if (st != CCQ_OK || M == 0 || m->rows == 0) return st;
   if (!gemm_supported(m, M))
     return fail(CCQ_ERR_CONFIG, "tcgen05 GEMM needs group_size 64 and cols % 64 == 0");
+  DeviceScope ds(m->device);
   return launch_gemm(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
 }
 
@@ -496,6 +499,7 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
   if (M < 0) return fail(CCQ_ERR_SHAPE, "negative batch");
   int st = check_dtypes(x_dtype, y_dtype);
   if (st != CCQ_OK || M == 0 || m->rows == 0) return st;
+  DeviceScope ds(m->device);
   // Dispatch by batch (measured, profiles/r01_sweep.json): M = 1 on the
   // CUDA-core streaming GEMV; 2 <= M <= 8 (2.06: see below; bf16/f16 activations) on the
   // tensor-pipe GEMV when all tokens fit one launch; the tcgen05 GEMM above
@@ -528,15 +532,6 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
 // ---- synchronous host-buffer entry points ----
 
 namespace {
-
-struct DeviceScope {
-  int prev = 0;
-  explicit DeviceScope(int d) {
-    cudaGetDevice(&prev);
-    cudaSetDevice(d);
-  }
-  ~DeviceScope() { cudaSetDevice(prev); }
-};
 
 // Scratch for the synchronous host entry points: stream-ordered allocations
 // from the library pool on the legacy stream (no cudaMalloc per call).

@@ -115,6 +115,8 @@ extern "C" int ccq_cuda_moe_forward(const ccq_dev_model* stack, const int32_t* t
   const int64_t K = stack->cols, N = stack->rows_per_expert, pairs = T * k;
   const int64_t xb = x_dtype == CCQ_DTYPE_F32 ? 4 : 2;
   if ((K * xb) % 16 != 0) return fail(CCQ_ERR_SHAPE, "activation rows must be a multiple of 16 bytes");
+  if (reinterpret_cast<uintptr_t>(x) & 15u) return fail(CCQ_ERR_CONFIG, "activations must be 16-byte aligned");
+  DeviceScope ds(stack->device);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;

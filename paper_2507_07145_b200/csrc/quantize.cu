@@ -415,11 +415,8 @@ extern "C" int ccq_cuda_search_codes(const float* targets, int64_t n, int32_t va
   int dev = 0;
   cudaGetDevice(&dev);
   const int64_t blocks = std::min<int64_t>((n + wpb - 1) / wpb, int64_t(num_sms(dev)) * 16);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && configured < smem) {
-    CCQ_CUDA_TRY(cudaFuncSetAttribute(search_codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-  }
+  if (smem > 48 * 1024)
+    if (int st = ensure_smem(reinterpret_cast<const void*>(search_codes_kernel), smem)) return st;
   search_codes_kernel<<<unsigned(blocks), wpb * 32, smem, static_cast<cudaStream_t>(stream)>>>(
       targets, n, valid, stride, scales, zero_point, L, N, S, codes);
   count_launch();

@@ -11,6 +11,13 @@
 //
 //   ccq_gpu_bench [--shapes 4096x4096,4096x14336] [--m 1,4,16] [--bpw 2.06|2.5|2.75]
 //                 [--iters 20] [--seed 1]
+//
+// `ccq_gpu_bench bench [...]` is the reference CLI's `ccq bench` itself
+// (ccq_main.cpp:241-277, same options and defaults: --shapes
+// 4096x4096,4096x1024,8192x8192,8192x1024 --m 1,4 --bpw 2.75 --group-size 64
+// --iters 5 --seed 1 --out PATH): ccq::bench_model rows for every shape, the
+// reference's three variants plus ccq_gpu_fused.  It is what acceptance
+// criterion 10 drives through CCQ_BIN (tests/test_acceptance.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -95,7 +102,64 @@ double median_ms(int iters, F&& body) {
 
 }  // namespace
 
+// The reference CLI's bench subcommand on ccq::bench_model.
+int cmd_bench(int argc, char** argv) {
+  std::string shapes = "4096x4096,4096x1024,8192x8192,8192x1024", ms = "1,4", bpw = "2.75", out;
+  int iters = 5, group_size = 64;
+  std::uint64_t seed = 1;
+  for (int i = 2; i < argc; i += 2) {
+    const std::string k = argv[i];
+    if (i + 1 >= argc) {
+      std::fprintf(stderr, "option %s needs a value\n", k.c_str());
+      return 2;
+    }
+    const std::string v = argv[i + 1];
+    if (k == "--shapes") shapes = v;
+    else if (k == "--m") ms = v;
+    else if (k == "--bpw") bpw = v;
+    else if (k == "--group-size") group_size = std::atoi(v.c_str());
+    else if (k == "--iters") iters = std::atoi(v.c_str());
+    else if (k == "--seed") seed = std::strtoull(v.c_str(), nullptr, 10);
+    else if (k == "--out") out = v;
+    else {
+      std::fprintf(stderr, "unknown option %s\n", k.c_str());
+      return 2;
+    }
+  }
+  try {
+    if (group_size != 64) throw ccq::ConfigError("ccq_gpu_bench models use group_size 64");
+    const ccq::Family fam = ccq::family_from_name(bpw);
+    std::vector<int> batches;
+    for (const auto& b : split(ms, ',')) batches.push_back(std::atoi(b.c_str()));
+    if (batches.empty()) throw ccq::ConfigError("no batch sizes given");
+    std::vector<ccq::BenchRow> rows;
+    for (const auto& sh : split(shapes, ',')) {
+      const auto dims = split(sh, 'x');
+      if (dims.size() != 2) throw ccq::ConfigError("shape must be AxB, got '" + sh + "'");
+      const std::int64_t d_in = std::atoll(dims[0].c_str()), d_out = std::atoll(dims[1].c_str());
+      if (d_in <= 0 || d_out <= 0) throw ccq::ConfigError("shape must be positive, got '" + sh + "'");
+      const ccq::PackedModel model = random_model(d_out, d_in, fam, seed + std::uint64_t(d_in) * 31 + d_out);
+      const auto r = ccq::bench_model(model, batches, iters, seed);
+      rows.insert(rows.end(), r.begin(), r.end());
+    }
+    const std::string csv = ccq::bench_csv(rows);
+    if (out.empty()) {
+      std::fputs(csv.c_str(), stdout);
+    } else {
+      FILE* f = std::fopen(out.c_str(), "w");
+      if (!f) throw ccq::Error("cannot open " + out + " for writing");
+      std::fputs(csv.c_str(), f);
+      std::fclose(f);
+    }
+  } catch (const ccq::Error& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 2;
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "bench") return cmd_bench(argc, argv);
   std::string shapes = "4096x4096", ms = "1,4,16", bpw = "2.06";
   int iters = 20;
   std::uint64_t seed = 1;
