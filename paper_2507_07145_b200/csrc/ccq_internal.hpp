@@ -253,6 +253,12 @@ int launch_grouped_stream(const ccq_dev_model* st, int E, int64_t rows_e, const 
 int launch_grouped_gemv(const ccq_dev_model* st, int E, int64_t rows_e, const int32_t* offsets_dev,
                         const int32_t* offsets_host, int64_t T, const void* x, int x_dtype, void* y,
                         int y_dtype, cudaStream_t s);
+// Small-batch (M <= 8) tensor-pipe GEMV over shared-memory-resident weights
+// (gemv_hmma.cu); kNotApplicable when the shape does not suit it.
+constexpr int kNotApplicable = -1;
+bool gemv_hmma_supported(const ccq_dev_model* m, int64_t M, int x_dtype, const void* x);
+int launch_gemv_hmma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+                     cudaStream_t s);
 int launch_gemv_mma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                     int y_dtype, cudaStream_t s);
 int num_sms(int device);

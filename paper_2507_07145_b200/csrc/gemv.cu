@@ -706,6 +706,176 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Resident-prefetch GEMV (M = 1): the latency-hiding variant for chains of
+// decode GEMVs.
+//
+// A token's GEMV chain is x-dependent but its WEIGHTS are not, and on B200
+// the 2.06 decode (not HBM) bounds the loop.  So each CTA is kept small
+// (8 warps, <= ~113 KB shared memory, <= 128 registers) to let TWO CTAs share
+// an SM: while layer i decodes, layer i+1's CTA is already resident (PDL),
+// has bulk-copied as much of its weight slice as fits into shared memory and
+// waits in griddepcontrol.wait.  The HBM stream of layer i+1 therefore
+// overlaps layer i's decode; after the wait only x (L1/L2), the decode of
+// shared-memory-resident records and a short fixed-order epilogue remain.
+// Tiles beyond the ring capacity stream through the same ring (refilled as
+// consumed).  Activations go straight from global memory to registers (no
+// shared-memory staging, no block barrier before the loop).
+// ---------------------------------------------------------------------------
+struct ResArgs {
+  DevLayout L;
+  const void* x;
+  void* y;
+  int y_dtype;
+  int streams;            // row streams per CTA (warps = nch * streams)
+  int S;                  // ring stages per warp
+  int rows_per_cta_max;
+};
+
+template <int FAM, int XDT>
+__device__ __forceinline__ void load_group_x_reg(const void* xin, int64_t g, XGroup<FAM, true>& xg) {
+  using T = G64<FAM>;
+  float xr[64];
+  load_x64<XDT>(xin, g * 64, xr);
+#pragma unroll
+  for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const int p = T::perm(i);
+    float4& f = xg.v[p >> 2];
+    if ((p & 3) == 0) f.x = xr[i];
+    else if ((p & 3) == 1) f.y = xr[i];
+    else if ((p & 3) == 2) f.z = xr[i];
+    else f.w = xr[i];
+  }
+}
+
+template <int FAM, int RPW, int XDT>
+__global__ void __launch_bounds__(256, 2) gemv_res(ResArgs a) {
+  using T = G64<FAM>;
+  constexpr bool SIDE = FAM == kF206;
+  constexpr int CGB = (32 * T::PB + 15) & ~15;
+  constexpr int REC = CGB + (SIDE ? 32 : 0);
+  constexpr int SB = RPW * REC;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const DevLayout& L = a.L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int nch = L.nch, S = a.S;
+  const int c = warp % nch, stream = warp / nch;
+  const int64_t r_begin = int64_t(blockIdx.x) * L.rows / gridDim.x;
+  const int64_t r_end = int64_t(blockIdx.x + 1) * L.rows / gridDim.x;
+  const int nrows = int(r_end - r_begin);
+  const int64_t w_begin = r_begin + int64_t(stream) * nrows / a.streams;
+  const int64_t w_end = r_begin + int64_t(stream + 1) * nrows / a.streams;
+  const int ntl = int((w_end - w_begin + RPW - 1) / RPW);
+
+  float* part = reinterpret_cast<float*>(smem);
+  uint8_t* rings = smem + ((size_t(a.rows_per_cta_max) * nch * 4 + 127) & ~size_t(127));
+  uint8_t* ring = rings + size_t(warp) * S * SB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rings + size_t(nwarps) * S * SB) + warp * S;
+
+  // 1. Weights first: they do not depend on the previous kernel.
+  const uint8_t* src = L.record(c, 0);
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int t, int s) {
+    const int64_t r0 = w_begin + int64_t(t) * RPW;
+    const uint32_t nr = uint32_t(w_end - r0 < RPW ? w_end - r0 : RPW);
+    mbar_arrive_expect_tx(&bars[s], nr * REC);
+    bulk_g2s_evict_first(ring + size_t(s) * SB, src + r0 * REC, nr * REC, &bars[s], pol);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    const int pre = ntl < S ? ntl : S;
+    for (int t = 0; t < pre; ++t) issue(t, t);
+  }
+  __syncwarp();
+  griddep_launch_dependents();
+  griddep_wait();  // x (and y) belong to the previous kernel until here
+
+  // 2. This lane's group of activations -> registers; Q = sum (class + zp) x.
+  const int g0 = c * kChunk;
+  const int ng = int(L.gpr - g0 < kChunk ? L.gpr - g0 : kChunk);
+  const bool active = lane < ng;
+  XGroup<FAM, true> xg;
+  float q = 0.f;
+  if (active) {
+    load_group_x_reg<FAM, XDT>(a.x, g0 + lane, xg);
+    float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      if (T::exact_tail(i)) continue;
+      const int p = T::perm(i);
+      const float4 f = xg.v[p >> 2];
+      const float xv = (p & 3) == 0 ? f.x : (p & 3) == 1 ? f.y : (p & 3) == 2 ? f.z : f.w;
+      q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xv, q4[i & 3]);
+    }
+    q = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  uint32_t one;
+  asm volatile("mov.b32 %0, 0x3f800000;" : "=r"(one));
+
+  // 3. Decode the resident (and streamed) tiles.
+#pragma unroll 1
+  for (int t = 0; t < ntl; ++t) {
+    const int s = t % S;
+    const int64_t r0 = w_begin + int64_t(t) * RPW;
+    float acc[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) acc[i] = 0.f;
+    mbar_wait(&bars[s], uint32_t((t / S) & 1));
+    const uint8_t* st = ring + size_t(s) * SB;
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const uint8_t* gp = st + r * REC + lane * T::PB;
+        float sc, dot;
+        if constexpr (FAM == kF206) {
+          const uint4 pv = lds128(st + r * REC + CGB + 16);
+          WidenPlan pl;
+          pl.C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
+          pl.M = pv.z;
+          pl.sel = pv.w;
+          const uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
+          const uint32_t sel[4] = {base, base + step, base + 2 * step, base + 3 * step};
+          const uint8_t nib = st[r * REC + CGB + (lane >> 1)];
+          sc = float((nib >> (4 * (lane & 1))) & 0xF);
+          dot = dot_206(gp, xg, q, pl, sel, one);
+        } else if constexpr (FAM == kF275) {
+          dot = dot_275(gp, xg, q, one, &sc);
+        } else {
+          dot = dot_25(gp, xg, q, one, &sc);
+        }
+        acc[r] = sc * dot;
+      }
+    }
+    if (t + S < ntl) {  // refill this stage (tiles beyond the ring capacity)
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) issue(t + S, s);
+    }
+    const float v = reduce_multi<RPW>(acc, lane);
+    constexpr int SPAN = 32 / RPW;
+    if ((lane & (SPAN - 1)) == 0) {
+      const int r = lane / SPAN;
+      if (r0 + r < w_end) part[int(r0 + r - r_begin) * nch + c] = v;
+    }
+  }
+  __syncthreads();
+  // 4. Fixed-order sum over chunks, row super scale, one write per row.
+  for (int rl = threadIdx.x; rl < nrows; rl += blockDim.x) {
+    float v = 0.f;
+    for (int cc = 0; cc < nch; ++cc) v += part[rl * nch + cc];
+    const int64_t row = r_begin + rl;
+    v *= L.super[row];
+    if (a.y_dtype == CCQ_DTYPE_F32) static_cast<float*>(a.y)[row] = v;
+    else static_cast<__nv_bfloat16*>(a.y)[row] = __float2bfloat16_rn(v);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic fallback for any group geometry / token count: one warp per row,
 // lanes stride over groups, exact per-weight decode (kernels.cpp:60-93).
 // ---------------------------------------------------------------------------
@@ -841,6 +1011,77 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemv launch");
 }
 
+// Shared memory one CTA may use so that two CTAs fit on an SM.
+int half_sm_smem(int dev) {
+  static int cached[64] = {0};
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int per_sm = 0, reserved = 0;
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    if (per_sm <= 0) per_sm = 233472;
+    cached[dev] = per_sm / 2 - reserved;
+  }
+  return cached[dev];
+}
+
+// Resident-prefetch GEMV launch (M = 1, nch <= 8).  Returns kNotApplicable when the
+// shape does not suit it (the caller takes the streaming kernel).
+template <int FAM, int RPW, int XDT>
+int launch_res_dt(const ccq_dev_model* m, const void* x, void* y, int y_dtype, cudaStream_t s) {
+  using T = G64<FAM>;
+  constexpr int CGB = (32 * T::PB + 15) & ~15;
+  constexpr int REC = CGB + (FAM == kF206 ? 32 : 0);
+  constexpr int SB = RPW * REC;
+  if (m->rec != uint32_t(REC) || m->nch > 8) return kNotApplicable;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ResArgs a{};
+  a.L = layout_of(m);
+  a.x = x;
+  a.y = y;
+  a.y_dtype = y_dtype;
+  const int64_t grid = std::min<int64_t>(num_sms(dev), m->rows);
+  a.rows_per_cta_max = int((m->rows + grid - 1) / grid);
+  a.streams = std::max(1, 8 / m->nch);
+  const int warps = m->nch * a.streams;
+  const int64_t rows_per_stream = (a.rows_per_cta_max + a.streams - 1) / a.streams;
+  const int need = int((rows_per_stream + RPW - 1) / RPW);
+  const size_t pbytes = (size_t(a.rows_per_cta_max) * m->nch * 4 + 127) & ~size_t(127);
+  const int budget = half_sm_smem(dev);
+  const int cap = int((int64_t(budget) - int64_t(pbytes) - 128) / (int64_t(warps) * (SB + 8)));
+  if (cap < 2) return kNotApplicable;
+  a.S = std::min(cap, std::max(need, 1));
+  const size_t smem = pbytes + size_t(warps) * a.S * (SB + 8) + 128;
+  auto kern = gemv_res<FAM, RPW, XDT>;
+  if (int st = ensure_smem(reinterpret_cast<const void*>(kern), smem)) return st;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(warps * 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  count_launch();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemv launch");
+}
+
+template <int FAM>
+int launch_res(const ccq_dev_model* m, const void* x, int x_dtype, void* y, int y_dtype, cudaStream_t s) {
+  static const bool off = !(std::getenv("CCQ_GEMV_RES") && std::atoi(std::getenv("CCQ_GEMV_RES")) == 1);
+  if (off) return kNotApplicable;
+  switch (x_dtype) {
+    case CCQ_DTYPE_F32: return launch_res_dt<FAM, 4, CCQ_DTYPE_F32>(m, x, y, y_dtype, s);
+    case CCQ_DTYPE_BF16: return launch_res_dt<FAM, 4, CCQ_DTYPE_BF16>(m, x, y, y_dtype, s);
+    default: return launch_res_dt<FAM, 4, CCQ_DTYPE_F16>(m, x, y, y_dtype, s);
+  }
+}
+
 template <int FAM, int RPW, int MT, int S>
 int launch_stream(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
                   void* y, int y_dtype, cudaStream_t s) {
@@ -867,7 +1108,9 @@ int launch_fam(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
       m0 += 2;
     } else {
       static const int rpw = std::getenv("CCQ_GEMV_RPW") ? std::atoi(std::getenv("CCQ_GEMV_RPW")) : 4;
-      if (rpw == 2) st = launch_stream<FAM, 2, 1, 6>(m, x, x_dtype, m0, 1, y, y_dtype, s);
+      if (M == 1 && (st = launch_res<FAM>(m, x, x_dtype, y, y_dtype, s)) != kNotApplicable) {
+        // resident-prefetch kernel took it
+      } else if (rpw == 2) st = launch_stream<FAM, 2, 1, 6>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       else if (rpw == 1) st = launch_stream<FAM, 1, 1, 8>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       else st = launch_stream<FAM, 4, 1, 3>(m, x, x_dtype, m0, 1, y, y_dtype, s);
       m0 += 1;
@@ -959,6 +1202,10 @@ int launch_grouped_stream(const ccq_dev_model* st, int E, int64_t rows_e, const 
 
 int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
+  if (gemv_hmma_supported(m, M, x_dtype, x)) {
+    const int st = launch_gemv_hmma(m, x, x_dtype, M, y, y_dtype, s);
+    if (st != kNotApplicable) return st;
+  }
   if (x_dtype != CCQ_DTYPE_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && M >= mma_min_tokens() &&
       gemv_mma_supported(m, M))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, s);

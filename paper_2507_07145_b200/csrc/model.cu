@@ -521,6 +521,10 @@ int ccq_cuda_matmul(const ccq_dev_model* m, const void* x, int x_dtype, int64_t 
     const int64_t splits = tiles * 2 <= sms && cblocks >= 8 ? std::min<int64_t>(sms / tiles, cblocks / 4) : 1;
     gemm_earlier = tiles * std::max<int64_t>(splits, 1) * 4 >= int64_t(sms) * 3;
   }
+  if (M >= 2 && gemv_hmma_supported(m, M, x_dtype, x)) {
+    const int hs = launch_gemv_hmma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
+    if (hs != kNotApplicable) return hs;
+  }
   if (mma && M >= mma_min_tokens() &&
       ((gemv_mma_fits(m, M) && !(gemm_earlier && gemm_supported(m, M))) || !gemm_supported(m, M)))
     return launch_gemv_mma(m, x, x_dtype, M, y, y_dtype, static_cast<cudaStream_t>(stream));
