@@ -37,7 +37,8 @@ WORKLOAD = "configs[1] Llama-3-8B MLP-up linear d_in 4096 -> d_out 14336, CCQ 2.
 def base_config(layers):
     """The workload description shared by both arms (same keys, same values)."""
     return {"workload": WORKLOAD, "d_in": D_IN, "d_out": D_OUT, "family": "2.06", "batch": M_HEAD,
-            "layers_per_step": layers}
+            "layers_per_step": layers, "weights": "random_quantized distribution (synthetic.cpp:25-103)",
+            "activations": "Gaussian, bf16-rounded"}
 
 
 def load_peaks():
@@ -130,8 +131,10 @@ def run_reference(args, world, rank):
     return {"metric": METRIC, "value": gbs, "unit": "GB/s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (random_quantized, Gaussian x)",
-            "config": dict(base_config(args.layers), parallelism="reference CPU path, host threads"),
+            "vs_baseline": None, "dtype": "f32 activations x CCQ codes, f64 accumulate (reference)",
+            "data": "synthetic (random_quantized, Gaussian x)",
+            "config": base_config(args.layers),
+            "arm": "reference CPU path (oracle/_ref gemv_batch), row-sharded over host threads",
             "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
                              "sample": sample},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -172,6 +175,7 @@ def main():
     ap.add_argument("--layers", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="add an M / family sweep")
+    ap.add_argument("--no-gemm", action="store_true", help="skip the batched GEMV/GEMM block")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -232,13 +236,17 @@ def main():
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         with torch.cuda.stream(stream):
             start.record(stream)
-            for _ in range(args.steps):
+            step_ev[0].record(stream)
+            for i in range(args.steps):
                 graph.replay()
+                step_ev[i + 1].record(stream)
             end.record(stream)
         torch.cuda.synchronize()
+    step_ms = sorted(step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps))
     barrier()
     ms = start.elapsed_time(end) / args.steps
     if world > 1:
@@ -316,8 +324,10 @@ def main():
         e2e_ms = float(t.item())
     e2e_val = bytes_step * world / (e2e_ms * 1e-3) / 1e9
 
-    sweep = prefill = moe = paper = None
+    sweep = prefill = moe = paper = gemm = None
     tflops_peak = float(peaks.get("bf16_tflops", 1590.0))
+    if rank == 0 and world == 1 and not args.no_gemm:
+        gemm = run_gemm_block(P, torch, dev, stream, hbm_peak, tflops_peak, local)
     if args.sweep and rank == 0:
         sweep = run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak)
         paper = run_paper_shapes(P, torch, dev, stream)
@@ -342,13 +352,14 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16 activations x CCQ codes, f32 accumulate",
             "data": "synthetic: random_quantized CCQ 2.06 weights (synthetic.cpp:25-103), "
                     "Gaussian bf16 activations",
-            "config": dict(base_config(args.layers),
-                           l2=f"inputs larger than L2: {args.layers} resident layer copies = "
-                              f"{bytes_step/1e6:.0f} MB rotated per step",
-                           parallelism=f"replicas x{world}"),
+            "config": base_config(args.layers),
+            "arm": f"B200 kernels, replicas x{world}",
+            "l2": f"inputs larger than L2: {args.layers} resident layer copies = "
+                  f"{bytes_step/1e6:.0f} MB rotated per step",
             "hbm_fraction": value / world / hbm_peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
@@ -362,7 +373,11 @@ def main():
                     "ms_per_step": e2e_ms},
             "gpu_launches": kernels_per_step * args.steps,
             "clocks": clk.summary(),
+            "step_ms": {"median": statistics.median(step_ms), "p10": step_ms[len(step_ms) // 10],
+                        "p90": step_ms[(9 * len(step_ms)) // 10], "n": len(step_ms)},
         }
+        if gemm is not None:
+            out["gemm"] = gemm
         if cpu is not None:
             out["cpu_baseline"] = cpu
         if sweep is not None:
@@ -377,6 +392,68 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def _l2_cold_us(P, torch, dev, stream, models, x, y, reps=10):
+    """us per call, graph-replayed over `models` (enough copies to exceed L2)."""
+    def body():
+        for mm in models:
+            P.matmul(mm, x, out=y, stream=stream)
+    return _graph_time_us(torch, stream, body, reps=reps) / len(models)
+
+
+def run_gemm_block(P, torch, dev, stream, hbm_peak, tflops_peak, local):
+    """The metric's second half ("GEMM TFLOP/s at batch 1-256") in the default
+    run: configs[1] 4096->14336 at M = 2..256 (all families at 16 and 256),
+    configs[4] prefill 8192->28672 M = 4096 (three families) and the ERNIE /
+    DeepSeek grouped prefill (configs[2] / [3], T = 4096 tokens, top-8).
+    Graph- or event-timed on the device, L2-cold, clocks sampled."""
+    import numpy as np
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    out = {"tensor_peak_tflops": tflops_peak, "hbm_peak_gbs": hbm_peak,
+           "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / hbm_gbs"}
+    with ClockSampler(local) as clk:
+        rows = []
+        for fam, fname, Ms in ((2, "2.06", (2, 4, 8, 16, 64, 256)), (0, "2.75", (16, 256)), (1, "2.5", (16, 256))):
+            copies = 12
+            ms_ = [P.DeviceModel.upload(_synthetic(D_OUT, D_IN, fam, 64, 31 + c), device=dev.index)
+                   for c in range(copies)]
+            pb = ms_[0].payload_bytes
+            for M in Ms:
+                x = torch.randn(M, D_IN, device=dev).to(torch.bfloat16)
+                y = torch.empty(M, D_OUT, device=dev)
+                us = _l2_cold_us(P, torch, dev, stream, ms_, x, y)
+                tf = 2 * M * D_IN * D_OUT / us / 1e6
+                rows.append({"config": "configs[1]", "family": fname, "d_in": D_IN, "d_out": D_OUT, "M": M,
+                             "us": round(us, 3), "packed_GBps": round(pb / us / 1e3, 1),
+                             "hbm_frac": round(pb / us / 1e3 / hbm_peak, 4), "TFLOPs": round(tf, 2),
+                             "tensor_frac": round(tf / tflops_peak, 4)})
+            del ms_
+        out["configs1"] = rows
+        out["configs4_prefill"] = run_prefill(P, torch, dev, stream, tflops_peak)
+        moe = []
+        for name, E, din, dout in (("ERNIE-4.5-300B-A47B", 64, 8192, 3584), ("DeepSeek-V3", 256, 7168, 2048)):
+            ex = P.Experts.upload([_synthetic(dout, din, 2, 64, 1000 + e) for e in range(E)], device=dev.index)
+            rng = np.random.default_rng(7)
+            counts = np.zeros(E, np.int64)
+            for _ in range(4096):
+                counts[rng.choice(E, 8, replace=False)] += 1
+            offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+            T = int(offs[-1])
+            offs_dev = torch.from_numpy(offs).to(dev)
+            x = torch.randn(T, din, device=dev).to(torch.bfloat16)
+            y = torch.empty(T, dout, device=dev, dtype=torch.bfloat16)
+            us = _graph_time_us(torch, stream, lambda: P.experts_matmul(ex, offs, x, out=y, stream=stream,
+                                                                          offsets_dev=offs_dev), reps=5)
+            tf = 2 * T * din * dout / us / 1e6
+            moe.append({"config": "configs[2]" if E == 64 else "configs[3]", "model": name, "experts": E,
+                        "d_in": din, "d_out": dout, "tokens": 4096, "routed_pairs": T, "us": round(us, 1),
+                        "TFLOPs": round(tf, 1), "tensor_frac": round(tf / tflops_peak, 4)})
+            del ex, x, y
+            torch.cuda.empty_cache()
+        out["moe_prefill"] = moe
+    out["clocks"] = clk.summary()
+    return out
 
 
 def run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak):

@@ -30,6 +30,10 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+    # both arms describe the workload with the same config dict (same_config)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.base_config(12)
 
 
 @pytest.mark.gpu
@@ -45,3 +49,13 @@ def test_product_arm_json_line(cuda):
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert "workload" in d["config"]
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.base_config(12)
+    g = d["gemm"]  # the metric's second half: batched GEMV / GEMM TFLOP/s
+    assert {r["M"] for r in g["configs1"] if r["family"] == "2.06"} == {2, 4, 8, 16, 64, 256}
+    assert all(r["TFLOPs"] > 0 and 0 < r["tensor_frac"] < 1 for r in g["configs1"])
+    assert {r["family"] for r in g["configs4_prefill"]} == {"2.06", "2.75", "2.5"}
+    assert all(0 < r["tensor_frac"] < 1 for r in g["configs4_prefill"] + g["moe_prefill"])
+    assert {r["config"] for r in g["moe_prefill"]} == {"configs[2]", "configs[3]"}
+    assert "sm_mhz" in g["clocks"]

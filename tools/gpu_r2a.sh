@@ -1,4 +1,4 @@
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+s=$(date +%s.%N); timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; e=$(date +%s.%N); echo "bench wall $(echo "$e - $s" | bc) s" >> $OUT/bench.err
