@@ -512,11 +512,14 @@ def test_config4_shape_decode_batches_full_size(oracle, ccq, cuda, fam):
 
 
 @pytest.mark.parametrize("name,E,din,dout,B", [("ERNIE", 64, 8192, 3584, 1), ("ERNIE", 64, 8192, 3584, 64),
-                                               ("DeepSeek", 256, 7168, 2048, 1), ("DeepSeek", 256, 7168, 2048, 16)])
+                                               ("DeepSeek", 256, 7168, 2048, 1), ("DeepSeek", 256, 7168, 2048, 16),
+                                               ("ERNIE", 64, 8192, 3584, 4096), ("DeepSeek", 256, 7168, 2048, 4096)])
 def test_moe_configs_full_size_sampled(oracle, ccq, cuda, name, E, din, dout, B):
-    """BASELINE configs[2]/[3] at full expert count and shape, top-8 routing:
-    every routed expert's output rows checked against the oracle for the
-    experts on a sample (all for B=1)."""
+    """BASELINE configs[2]/[3] at full expert count and shape, top-8 routing,
+    decode batches and the T = 4096-token prefill (32,768 routed pairs on the
+    grouped tcgen05 GEMM): routed experts' output rows checked against the
+    oracle (B = 4096: three experts, 48 of their tokens each - the CPU
+    oracle is f64)."""
     torch = cuda
     rng = np.random.default_rng(B + E)
     counts = np.zeros(E, np.int64)
@@ -528,9 +531,11 @@ def test_moe_configs_full_size_sampled(oracle, ccq, cuda, name, E, din, dout, B)
     x = bf16_round(oracle.random_matrix(int(offs[-1]), din, "gaussian", 11))
     y = ccq.experts_matmul(ex, offs, torch.from_numpy(x).to("cuda").to(torch.bfloat16)).cpu().numpy()
     hit = [e for e in range(E) if counts[e]]
-    for e in hit[:8]:
-        want = oracle.gemv_batch(secs[e], x[offs[e]:offs[e + 1]], threads=8)
-        assert rel_err(y[offs[e]:offs[e + 1]], want) < REL_TOL, (name, e)
+    sample = hit[:8] if B < 4096 else [hit[0], hit[len(hit) // 2], hit[-1]]
+    for e in sample:
+        t1 = offs[e + 1] if B < 4096 else min(offs[e + 1], offs[e] + 48)
+        want = oracle.gemv_batch(secs[e], x[offs[e]:t1], threads=8)
+        assert rel_err(y[offs[e]:t1], want) < REL_TOL, (name, e)
 
 
 # ----------------------------------------------------------- randomized sweep --
@@ -702,3 +707,39 @@ def test_experts_two_tokens_per_expert(oracle, ccq, cuda, fam, counts, rows, col
     y = ccq.experts_matmul(ex, offs, xt)
     torch.cuda.synchronize()
     assert rel_err(y.cpu().numpy(), want) < REL_TOL
+
+
+def test_config0_full_size_gaussian_quantized(oracle, ccq, cuda):
+    """BASELINE configs[0] as specified: a 4096 x 4096 Gaussian weight matrix
+    (the reference's random_matrix, mt19937_64 + Box-Muller) quantized to 2.06
+    bits (quantize_tensor, g = 64, rounds = 2) on the GPU, then decode and the
+    batch-1 GEMV against the CPU oracle.  The quantization itself is pinned
+    to the reference's own quantizer (oracle/_ref) on two 32-row slices (the
+    quantizer is row-independent), the decode is bit-exact over the whole
+    matrix and the M = 1 products (bf16 and f32 activations) are within the
+    reference's acceptance tolerance 1e-4 (acceptance_main.cpp:329-371)."""
+    torch = cuda
+    w = oracle.random_matrix(4096, 4096, "gaussian", 4096 * 31 + 4096).astype(np.float32)
+    got = ccq.quantize(w, 2, 64, 2)
+    s = oracle.Sections(got.rows, got.cols, got.family, got.group_size,
+                        np.asarray(got.code_payload, np.uint8), np.asarray(got.scale_payload, np.uint8),
+                        np.asarray(got.super_scales, np.float32), np.asarray(got.cluster_scales, np.float32),
+                        np.asarray(got.cluster_zero_points, np.float32))
+    if oracle.ref_available():
+        for r0 in (0, 2048):
+            want = oracle.RefModel.quantize(np.ascontiguousarray(w[r0:r0 + 32]), 2, 64, 2, threads=0).sections()
+            part = _slice_rows(oracle, s, r0, r0 + 32)
+            assert np.array_equal(part.code_payload, np.asarray(want.code_payload, np.uint8)), r0
+            assert np.array_equal(part.scale_payload, np.asarray(want.scale_payload, np.uint8)), r0
+            for a, b in ((part.super_scales, want.super_scales), (part.cluster_scales, want.cluster_scales),
+                         (part.cluster_zero_points, want.cluster_zero_points)):
+                assert np.array_equal(np.asarray(a, np.float32).view(np.uint32),
+                                      np.asarray(b, np.float32).view(np.uint32)), r0
+    d = ccq.DeviceModel.upload(got)
+    assert np.array_equal(ccq.dequantize(d).view(np.uint32), oracle.dequantize(s).view(np.uint32))
+    x = oracle.random_matrix(1, 4096, "uniform", 4096 * 31 + 4096)
+    for xin in (x, bf16_round(x)):
+        want = oracle.gemv_batch(s, xin, threads=8)
+        dt = torch.bfloat16 if xin is not x else torch.float32
+        y = ccq.matmul(d, torch.from_numpy(xin).to("cuda").to(dt)).cpu().numpy()
+        assert rel_err(y, want) < 1e-4

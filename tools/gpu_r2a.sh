@@ -1,4 +1,4 @@
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-s=$(date +%s.%N); timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; e=$(date +%s.%N); echo "bench wall $(echo "$e - $s" | bc) s" >> $OUT/bench.err
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "config0 or moe_configs_full" --durations=5 > $OUT/pytest_new.log 2>&1; echo "rc=$?" >> $OUT/pytest_new.log
