@@ -433,11 +433,20 @@ def experts_matmul(experts: "Experts", offsets, x, out=None, out_dtype=None, str
     return out
 
 
-def moe_forward(experts: "Experts", topk_ids, topk_weights, x, out=None, out_dtype=None, stream=None):
+def moe_forward(experts: "Experts", topk_ids, topk_weights, x, out=None, out_dtype=None, stream=None,
+                validate: bool = True):
     """MoE layer with routing (ccq_cuda_moe_forward): x[T, cols] in token order,
     topk_ids / topk_weights [T, k] on the device -> y[T, rows_per_expert] =
-    sum_j w[t, j] * expert_{ids[t, j]}(x[t])."""
+    sum_j w[t, j] * expert_{ids[t, j]}(x[t]).
+
+    The library call never synchronises (CUDA-graph capturable); with
+    validate=True (default) the ids are range-checked here first (one host
+    read), pass validate=False inside a captured serving loop."""
     import torch
+    if validate and topk_ids.numel():
+        lo, hi = int(topk_ids.min().item()), int(topk_ids.max().item())
+        if lo < 0 or hi >= experts.num_experts:
+            raise ShapeError(f"router expert id out of range [0, {experts.num_experts})")
     if topk_ids.dtype != torch.int32 or topk_weights.dtype != torch.float32:
         raise ShapeError("topk_ids must be int32 and topk_weights float32")
     if topk_ids.shape != topk_weights.shape or topk_ids.dim() != 2 or topk_ids.shape[0] != x.shape[0]:

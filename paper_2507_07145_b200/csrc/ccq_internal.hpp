@@ -236,6 +236,11 @@ int launch_gemv(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
 int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y,
                 int y_dtype, cudaStream_t s);
 bool gemm_supported(const ccq_dev_model* m, int64_t M);
+// Sync-free grouped GEMM over a device-side token-tile prefix (moe.cu).
+int grouped_tile_tokens(const ccq_dev_model* stack, int64_t pairs, int E, int x_dtype);
+int launch_grouped_gemm_tiles(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
+                              const int32_t* tile_prefix_dev, int64_t max_tiles, int64_t T, const void* x,
+                              int x_dtype, void* y, int y_dtype, cudaStream_t s);
 int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
                         int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
                         int y_dtype, cudaStream_t s);

@@ -234,6 +234,11 @@ struct GemmArgs {
   // raw f32 partials go to partial[z][token][row] and a reduce kernel scales them
   int kbs;
   float* partial;
+  // grouped tile-list mode (tile_prefix != nullptr): blockIdx.x is a global
+  // token-tile index; expert e owns tiles [tile_prefix[e], tile_prefix[e+1])
+  // (device-computed, so the launch needs no host copy of the routing)
+  const int32_t* tile_prefix;
+  int E;
 };
 
 __device__ __forceinline__ uint32_t lop_mask_or(uint32_t v, uint32_t mask, uint32_t magic) {
@@ -464,10 +469,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   int n0;
   const int tb = BN / a.xs;
   if (a.offsets) {
-    const int e = blockIdx.y / a.tpe, t = blockIdx.y % a.tpe;
+    int e, t, jt;
+    if (a.tile_prefix) {
+      const int tt = int(blockIdx.x);
+      if (tt >= a.tile_prefix[a.E]) return;  // worst-case grid: no tile here
+      int lo = 0, hi = a.E;                  // tile_prefix[lo] <= tt < tile_prefix[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= tt) lo = mid;
+        else hi = mid;
+      }
+      e = lo;
+      jt = tt - a.tile_prefix[e];
+      t = int(blockIdx.y);
+    } else {
+      e = blockIdx.y / a.tpe;
+      t = blockIdx.y % a.tpe;
+      jt = int(blockIdx.x);
+    }
     r0 = e * a.rows_e + int64_t(t) * kBM;
     row_end = (e + 1) * a.rows_e < r0 + kBM ? (e + 1) * a.rows_e : r0 + kBM;
-    n0 = a.offsets[e] + blockIdx.x * tb;
+    n0 = a.offsets[e] + jt * tb;
     tok_end = a.offsets[e + 1];
     if (n0 >= tok_end) return;  // expert without (more) tokens: no work, no bytes
     y_ld = a.rows_e;
@@ -824,7 +846,7 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ p
 template <int FAM, int BN>
 int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
             cudaStream_t s, const int32_t* offsets_dev = nullptr, int64_t rows_e = 0, int E = 0,
-            int64_t max_tokens = 0) {
+            int64_t max_tokens = 0, const int32_t* tile_prefix = nullptr, int64_t max_tiles = 0) {
   using SM = GemmSmem<FAM, BN>;
   const int64_t K = m->cols;
   const bool grouped = offsets_dev != nullptr;
@@ -876,14 +898,16 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
     return st;
   }
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
-             offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr};
+             offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr,
+             tile_prefix, E};
   auto kern = gemm_ccq<FAM, BN>;
   if (int st2 = ensure_smem(reinterpret_cast<const void*>(kern), SM::TOTAL)) {
     cudaFreeAsync(x16, s);
     return st2;
   }
   const int tb = BN / xs;
-  dim3 grid = grouped ? dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe))
+  dim3 grid = grouped ? (tile_prefix ? dim3(unsigned(max_tiles), unsigned(a.tpe))
+                                     : dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe)))
                       : dim3(unsigned((M + tb - 1) / tb), unsigned((m->rows + kBM - 1) / kBM));
   // Split K when the tiles would leave most SMs idle (K-heavy shapes such as
   // 14336 -> 4096: 32 row tiles); splits cover whole 8-group code blocks.
@@ -979,6 +1003,37 @@ int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const
       return CCQ_GROUPED(kF206, 256);
   }
 #undef CCQ_GROUPED
+}
+
+// Sync-free grouped GEMM: the routing lives only on the device.  tile_prefix
+// (E + 1 entries, written by an earlier kernel) counts token tiles of
+// grouped_tile_tokens(...) tokens per expert; the grid is sized for the worst
+// case (max_tiles) and CTAs past tile_prefix[E] exit at once.
+int grouped_tile_tokens(const ccq_dev_model* stack, int64_t pairs, int E, int x_dtype) {
+  const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
+  const int64_t avg = (pairs + E - 1) / std::max(E, 1) * xs;
+  int bn = avg > 96 ? 256 : (avg > 48 ? 128 : 64);
+  if (stack->family == kF25 && bn > 128) bn = 128;
+  return bn / xs;
+}
+
+int launch_grouped_gemm_tiles(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
+                              const int32_t* tile_prefix_dev, int64_t max_tiles, int64_t T, const void* x,
+                              int x_dtype, void* y, int y_dtype, cudaStream_t s) {
+  if (T <= 0 || max_tiles <= 0) return CCQ_OK;
+  const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
+  const int bn = grouped_tile_tokens(stack, T, E, x_dtype) * xs;
+#define CCQ_TILES(F, B) \
+  run_gemm<F, B>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, 0, tile_prefix_dev, max_tiles)
+  switch (stack->family) {
+    case kF275:
+      return bn == 64 ? CCQ_TILES(kF275, 64) : bn == 128 ? CCQ_TILES(kF275, 128) : CCQ_TILES(kF275, 256);
+    case kF25:
+      return bn == 64 ? CCQ_TILES(kF25, 64) : CCQ_TILES(kF25, 128);
+    default:
+      return bn == 64 ? CCQ_TILES(kF206, 64) : bn == 128 ? CCQ_TILES(kF206, 128) : CCQ_TILES(kF206, 256);
+  }
+#undef CCQ_TILES
 }
 
 }  // namespace ccqb

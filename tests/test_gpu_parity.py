@@ -592,6 +592,48 @@ def test_moe_forward_routing(oracle, ccq, cuda, fam, T, k, E):
     assert rel_err(y.cpu().numpy(), want) < REL_TOL
 
 
+@pytest.mark.parametrize("fam", [2, 0])
+def test_moe_forward_graph_capture_and_replay(oracle, ccq, cuda, fam):
+    """ccq_cuda_moe_forward never synchronises: it is captured once in a CUDA
+    graph and replayed with NEW routing and activations written into the
+    captured input buffers; every replay matches the oracle composition
+    (decode batch T = 4 and a prefill-sized batch T = 300, top-4 of 16)."""
+    torch = cuda
+    rows, cols, E, k = 64, 512, 16, 4
+    secs = [oracle.random_packed(rows, cols, fam, 64, seed=e + 900 + fam) for e in range(E)]
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(t) for t in secs])
+    for T in (4, 300):
+        ids_d = torch.zeros(T, k, dtype=torch.int32, device="cuda")
+        w_d = torch.zeros(T, k, dtype=torch.float32, device="cuda")
+        x_d = torch.zeros(T, cols, dtype=torch.bfloat16, device="cuda")
+        y_d = torch.empty(T, rows, dtype=torch.float32, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):  # warm-up (allocations, attributes) outside capture
+            ccq.moe_forward(ex, ids_d, w_d, x_d, out=y_d, stream=s, validate=False)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ccq.moe_forward(ex, ids_d, w_d, x_d, out=y_d, stream=s, validate=False)
+        for rep in range(3):
+            rng = np.random.default_rng(T * 7 + rep + fam)
+            ids = np.stack([rng.choice(E, k, replace=False) for _ in range(T)]).astype(np.int32)
+            w = rng.random((T, k)).astype(np.float32)
+            x = bf16_round(oracle.random_matrix(T, cols, "gaussian", T + rep))
+            ids_d.copy_(torch.from_numpy(ids))
+            w_d.copy_(torch.from_numpy(w))
+            x_d.copy_(torch.from_numpy(x).to(torch.bfloat16))
+            g.replay()
+            torch.cuda.synchronize()
+            want = np.zeros((T, rows), np.float64)
+            for e in range(E):
+                tok, slot = np.nonzero(ids == e)
+                if tok.size:
+                    ye = oracle.gemv_batch(secs[e], x[tok], threads=8)
+                    for i in range(tok.size):
+                        want[tok[i]] += float(w[tok[i], slot[i]]) * ye[i]
+            assert rel_err(y_d.cpu().numpy(), want) < REL_TOL, (T, rep)
+
+
 def test_moe_forward_rejects_bad_expert_ids(ccq, cuda):
     torch = cuda
     from paper_2507_07145_b200.synthetic import random_packed
