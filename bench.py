@@ -176,6 +176,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="add an M / family sweep")
     ap.add_argument("--no-gemm", action="store_true", help="skip the batched GEMV/GEMM block")
+    ap.add_argument("--chunk-tokens", type=int, default=1024, help="sharded GEMM all-gather chunk")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded configs[4]/[2] block also at N=1 (always on for N>1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -328,6 +331,9 @@ def main():
     tflops_peak = float(peaks.get("bf16_tflops", 1590.0))
     if rank == 0 and world == 1 and not args.no_gemm:
         gemm = run_gemm_block(P, torch, dev, stream, hbm_peak, tflops_peak, local)
+    sharded = None
+    if world > 1 or args.sharded:
+        sharded = run_sharded(P, torch, dev, stream, world, rank, local, tflops_peak, args)
     if args.sweep and rank == 0:
         sweep = run_sweep(P, torch, dev, stream, hbm_peak, tflops_peak)
         paper = run_paper_shapes(P, torch, dev, stream)
@@ -378,6 +384,8 @@ def main():
         }
         if gemm is not None:
             out["gemm"] = gemm
+        if sharded is not None:
+            out["sharded"] = sharded
         if cpu is not None:
             out["cpu_baseline"] = cpu
         if sweep is not None:
@@ -392,6 +400,102 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_sharded(P, torch, dev, stream, world, rank, local, tflops_peak, args):
+    """SURVEY 8e on the N GPUs of this job (strong scaling: the layer is fixed,
+    the work splits): configs[4] 8192 -> 28672 (2.06, M = 4096 prefill)
+    N-column sharded with the chunked decode-matmul + NCCL all-gather of
+    ccq_cuda_shard_allgather, and configs[2] (ERNIE 64 experts, T = 4096
+    tokens, top-8) expert-sharded with one output all-gather.  Device-timed,
+    max over ranks.  Also: compute-only and gather-only times."""
+    import numpy as np
+    import torch.distributed as dist
+    from paper_2507_07145_b200.parallel import NcclComm, ShardedExperts, ShardedLinear
+    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    out = {"n_gpus": world, "scaling": "strong", "tensor_peak_tflops_per_gpu": tflops_peak}
+    made_group = False
+    if world == 1 and not dist.is_initialized():
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+        made_group = True
+    comm = NcclComm(device=local)
+    with ClockSampler(local) as clk:
+        # configs[4]: N-column sharding + chunked all-gather
+        pk = _synthetic(28672, 8192, 2, 64, 5)
+        lin = ShardedLinear(pk, device=local, comm=comm)
+        del pk
+        g = torch.Generator(device="cpu").manual_seed(4097)
+        x = torch.randn(4096, 8192, generator=g).to(torch.bfloat16).to(dev)
+        y = torch.empty(4096, 28672, dtype=torch.bfloat16, device=dev)
+        yl = torch.empty(4096, lin.r1 - lin.r0, dtype=torch.bfloat16, device=dev)
+        flop = 2 * 4096 * 8192 * 28672
+        with torch.cuda.stream(stream):
+            ms = timed(lambda: lin(x, out=y, chunk_tokens=args.chunk_tokens, stream=stream), 5)
+            ms_c = timed(lambda: P.matmul(lin.local, x, out=yl, stream=stream), 5)
+            ms_g = None
+            if world > 1:
+                gath = torch.empty(world, 4096, lin.r1 - lin.r0, dtype=torch.bfloat16, device=dev)
+                ms_g = timed(lambda: dist.all_gather_into_tensor(gath, yl), 5)
+        out["configs4"] = {"d_in": 8192, "d_out": 28672, "M": 4096, "family": "2.06", "out_dtype": "bf16",
+                           "rows_per_gpu": lin.r1 - lin.r0, "chunk_tokens": args.chunk_tokens,
+                           "ms": round(ms, 4), "TFLOPs": round(flop / (ms * 1e-3) / 1e12, 1),
+                           "tensor_frac_per_gpu": round(flop / (ms * 1e-3) / 1e12 / world / tflops_peak, 4),
+                           "compute_only_ms": round(ms_c, 4),
+                           "gather_only_ms": None if ms_g is None else round(ms_g, 4),
+                           "gather_bytes_per_gpu": (world - 1) * 4096 * (lin.r1 - lin.r0) * 2}
+        del lin, x, y, yl
+        torch.cuda.empty_cache()
+        # configs[2]: expert sharding (ERNIE-4.5 64 x 8192 -> 3584, T = 4096, top-8)
+        E, din, dout = 64, 8192, 3584
+        from paper_2507_07145_b200.parallel import block_range
+        e0, e1 = block_range(E, rank, world)
+        sh = ShardedExperts.from_local([_synthetic(dout, din, 2, 64, 1000 + e) for e in range(e0, e1)], E, dout,
+                                       device=local)
+        rng = np.random.default_rng(7)
+        counts = np.zeros(E, np.int64)
+        for _ in range(4096):
+            counts[rng.choice(E, 8, replace=False)] += 1
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        T = int(offs[-1])
+        xe = torch.randn(T, din, generator=g).to(torch.bfloat16).to(dev)
+        with torch.cuda.stream(stream):
+            ms_e = timed(lambda: sh(offs, xe, out_dtype=torch.bfloat16), 3)
+        fl = 2 * T * din * dout
+        out["configs2"] = {"model": "ERNIE-4.5-300B-A47B", "experts": E, "experts_per_gpu": e1 - e0,
+                           "d_in": din, "d_out": dout, "tokens": 4096, "routed_pairs": T, "ms": round(ms_e, 4),
+                           "TFLOPs": round(fl / (ms_e * 1e-3) / 1e12, 1),
+                           "tensor_frac_per_gpu": round(fl / (ms_e * 1e-3) / 1e12 / world / tflops_peak, 4)}
+        del sh, xe
+    out["clocks"] = clk.summary()
+    comm.close()
+    if made_group:
+        dist.destroy_process_group()
+    return out if rank == 0 else None
 
 
 def _l2_cold_us(P, torch, dev, stream, models, x, y, reps=10):

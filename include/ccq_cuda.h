@@ -171,13 +171,36 @@ int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t* offsets_d
  * order, router top-k expert ids topk_ids[T x k] (device int32) and weights
  * topk_w[T x k] (device f32) -> y[T x rows_per_expert] =
  * sum_j topk_w[t,j] * (expert topk_ids[t,j]) x[t], summed in j order.
- * Permutes the routed rows expert-major, runs ccq_cuda_experts_matmul, and
- * combines.  Synchronises `stream` once (the grouped launch is sized from the
- * routing counts); not graph-capturable.  Expert ids outside [0, E) ->
- * CCQ_ERR_SHAPE. */
+ * Permutes the routed rows expert-major, runs the grouped tcgen05 GEMM over a
+ * device-side token-tile list, and combines.  Never synchronises: the whole
+ * call is stream-ordered and CUDA-graph capturable.  Expert ids outside
+ * [0, E) are dropped (those pairs contribute zero); validate ids upstream
+ * if they are untrusted. */
 int ccq_cuda_moe_forward(const ccq_dev_model* stack, const int32_t* topk_ids, const float* topk_w,
                          int64_t T, int32_t k, const void* x, int x_dtype, void* y, int y_dtype,
                          void* stream);
+
+/* ---- multi-GPU: output rows split across the ranks of a node ---- */
+
+/* NCCL is resolved at run time from the libnccl.so.2 already loaded in the
+ * process (e.g. torch's) or on the library path; no link-time dependency.
+ * ccq_nccl_unique_id: rank 0 creates the 128-byte id and shares it (any
+ * side channel); every rank then calls ccq_nccl_comm_init on its device. */
+int ccq_nccl_unique_id(uint8_t* out128);
+int ccq_nccl_comm_init(int world, int rank, const uint8_t* id128, int device, void** comm);
+int ccq_nccl_comm_destroy(void* comm);
+
+/* Row-sharded linear + output all-gather (the ccq_cuda_shard_allgather of
+ * SURVEY §8b).  `shard` holds this rank's block [rank*N/world,
+ * (rank+1)*N/world) of an N = rows_total row layer (ccq_cuda_model_upload_rows);
+ * y is the FULL output [M x rows_total] on every rank.  Tokens run in chunks of
+ * chunk_tokens (0 = all): chunk c's all-gather (NCCL, `comm` = ncclComm_t) and
+ * column interleave overlap chunk c+1's decode-matmul on a second stream;
+ * M = 1 with N % world == 0 gathers in place.  No host synchronisation (graph
+ * capturable).  world == 1 with comm == NULL is a plain ccq_cuda_matmul. */
+int ccq_cuda_shard_allgather(const ccq_dev_model* shard, int64_t rows_total, int world, int rank,
+                             const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+                             int64_t chunk_tokens, void* comm, void* stream);
 
 /* ---- synchronous host-buffer entry points (the reference signatures) ---- */
 

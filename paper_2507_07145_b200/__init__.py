@@ -103,7 +103,8 @@ ABI_SYMBOLS = [
     "ccq_gemv_host", "ccq_gemv_batch_host", "ccq_model_payload_bytes", "ccq_group_geometry",
     "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
     "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward", "ccq_cuda_search_codes",
-    "ccq_quantize_host", "ccq_cuda_quantize_model",
+    "ccq_quantize_host", "ccq_cuda_quantize_model", "ccq_nccl_unique_id", "ccq_nccl_comm_init",
+    "ccq_nccl_comm_destroy", "ccq_cuda_shard_allgather",
 ]
 
 _lib = None
@@ -140,6 +141,11 @@ def lib():
         L.ccq_cuda_search_codes.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i32, vp, vp]
         L.ccq_quantize_host.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.ccq_cuda_quantize_model.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp]
+        L.ccq_nccl_unique_id.argtypes = [vp]
+        L.ccq_nccl_comm_init.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
+        L.ccq_nccl_comm_destroy.argtypes = [vp]
+        L.ccq_cuda_shard_allgather.argtypes = [vp, i64, C.c_int, C.c_int, vp, C.c_int, i64, vp, C.c_int, i64,
+                                               vp, vp]
         L.ccq_dequantize_host.argtypes = [vp, vp]
         L.ccq_gemv_host.argtypes = [vp, vp, u64, vp, u64]
         L.ccq_gemv_batch_host.argtypes = [vp, vp, i64, i64, vp, i64, i64]

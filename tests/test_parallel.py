@@ -55,13 +55,14 @@ def _worker(rank, world, port, fam, rows, cols, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fam,rows", [(2, 37), (0, 64), (1, 33)])
-def test_row_sharded_gather_equals_unsharded(oracle, fam, rows):
+@pytest.mark.parametrize("fam,rows,world", [(2, 37, 2), (0, 64, 2), (1, 33, 2), (2, 37, 4), (0, 30, 4)])
+def test_row_sharded_gather_equals_unsharded(oracle, fam, rows, world):
+    """Row blocks over 2 and 4 ranks (uneven: 37 rows over 4 = 9/9/9/10)."""
     cols = 256
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, fam, rows, cols, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fam, rows, cols, q)) for r in range(world)]
     for p in procs:
         p.start()
     y = q.get(timeout=120)
@@ -148,5 +149,46 @@ def test_sharded_linear_and_experts_nccl_world1():
         got = ShardedExperts(exps, device=0)(offs, xe)
         want = P.experts_matmul(P.Experts.upload(exps), offs, xe)
         assert torch.equal(got, want)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_shard_allgather_library_nccl_world1():
+    """ccq_cuda_shard_allgather through a library-owned NCCL communicator
+    (world size 1 on the one GPU): the in-place M = 1 path and the chunked
+    path (all-gather + interleave on the second stream, 3 chunks, ragged last
+    chunk) equal the unsharded matmul bit for bit, f32 and bf16 outputs, and
+    the call can be captured in a CUDA graph."""
+    import paper_2507_07145_b200 as P
+    from paper_2507_07145_b200.parallel import NcclComm, ShardedLinear
+    from paper_2507_07145_b200.synthetic import random_packed
+    port = _free_port()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comm = NcclComm(device=0)
+        pk = random_packed(512, 1024, 2, 64, 6)
+        lin = ShardedLinear(pk, device=0, comm=comm)
+        full = P.DeviceModel.upload(pk)
+        for M, odt in ((1, torch.float32), (5, torch.bfloat16), (700, torch.float32)):
+            x = torch.randn(M, 1024, device="cuda").to(torch.bfloat16)
+            got = lin(x, out_dtype=odt, chunk_tokens=256)
+            torch.cuda.synchronize()
+            want = P.matmul(full, x, out_dtype=odt)
+            assert torch.equal(got, want), M
+        x = torch.randn(300, 1024, device="cuda").to(torch.bfloat16)
+        out = torch.empty(300, 512, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            lin(x, chunk_tokens=128, stream=s, out=out)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            lin(x, chunk_tokens=128, stream=s, out=out)
+        x.copy_(torch.randn(300, 1024, device="cuda").to(torch.bfloat16))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, P.matmul(full, x))
+        comm.close()
     finally:
         dist.destroy_process_group()
