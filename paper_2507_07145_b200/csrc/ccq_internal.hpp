@@ -134,6 +134,7 @@ struct DevLayout {
   const uint8_t* codes;  // record base
   const float* super;
   const WidenPlan* plan;
+  const double2* plan64;  // 2.06 FP64 widening plans (may be null)
   int64_t rows, cols, gpr, rows_pad;
   uint32_t cgb;  // code bytes per record
   uint32_t rec;  // bytes per (chunk, row) record
@@ -176,12 +177,17 @@ struct ccq_dev_model {
   int64_t rows_per_expert = 0;
   bool fast = false;           // group-64 streaming kernels apply
   int plan_pos_min = 0;        // 2.06: smallest byte position of any real row's widening plan
+  // 2.06: per-row FP64-pipe widening (A = 4096 alpha, B = beta + 1/2 - A as
+  // doubles): code = floor(fma.rm(1 + q 2^-12, A, B)); verified at upload for
+  // every valid q of every row (w64 = all rows exact).
+  double2* plan64 = nullptr;
+  bool w64 = false;
 };
 
 namespace ccqb {
 
 inline DevLayout layout_of(const ccq_dev_model* m) {
-  return DevLayout{m->codes, m->super, m->plan, m->rows, m->cols, m->gpr, m->rows_pad,
+  return DevLayout{m->codes, m->super, m->plan, m->plan64, m->rows, m->cols, m->gpr, m->rows_pad,
                    m->cgb, m->rec, m->nch, m->geo};
 }
 

@@ -920,8 +920,10 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = int64_t(grid.x) * grid.y;
     const int cblocks = int((m->gpr + 7) / 8);
-    if (!grouped && tiles > 0 && tiles * 2 <= sms && cblocks >= 8) {
+    static const int force_splits = std::getenv("CCQ_GEMM_SPLITS") ? std::atoi(std::getenv("CCQ_GEMM_SPLITS")) : 0;
+    if (!grouped && tiles > 0 && ((tiles * 2 <= sms && cblocks >= 8) || force_splits > 1)) {
       splits = int(std::min<int64_t>(sms / tiles, cblocks / 4));
+      if (force_splits > 1) splits = std::min(force_splits, cblocks);
       if (splits >= 2) {
         const int cb_per = (cblocks + splits - 1) / splits;
         a.kbs = cb_per * 8;
@@ -965,7 +967,9 @@ bool gemm_supported(const ccq_dev_model* m, int64_t M) {
 
 int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                 cudaStream_t s) {
-  const int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * M : M;  // BN is chosen on activation rows
+  int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * M : M;  // BN is chosen on activation rows
+  static const int force_bn = std::getenv("CCQ_GEMM_BN") ? std::atoi(std::getenv("CCQ_GEMM_BN")) : 0;
+  if (force_bn) xr = force_bn;
   switch (m->family) {
     case kF275:
       if (xr <= 64) return run_gemm<kF275, 64>(m, x, x_dtype, M, y, y_dtype, s);
@@ -987,7 +991,9 @@ int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const
                         int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
                         int y_dtype, cudaStream_t s) {
   if (max_tokens <= 0 || T <= 0) return CCQ_OK;
-  const int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * max_tokens : max_tokens;
+  int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * max_tokens : max_tokens;
+  static const int force_bn = std::getenv("CCQ_GROUPED_BN") ? std::atoi(std::getenv("CCQ_GROUPED_BN")) : 0;
+  if (force_bn) xr = force_bn;
 #define CCQ_GROUPED(F, B) run_gemm<F, B>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens)
   switch (stack->family) {
     case kF275:

@@ -234,6 +234,47 @@ __device__ __forceinline__ float dot_206(const uint8_t* gp, const X& x, float q,
   return fmaf(64.f, a0.x + a1.x, fmaf(512.f, a0.y + a1.y, -q));
 }
 
+// 2.06 with the widening on the FP64 pipe (plan64, model.cu build_plan64):
+// per byte one PRMT builds the high word of v = 1 + q 2^-12, fma.rm gives
+// t = floor-exact q alpha + beta + 1/2, and two add.rm with 2^44 / 2^38 leave
+// the code at bits [8,23) / [14,29) of the low word - the same `hi` /
+// `hi << 6` as the IMAD.WIDE plan, with the FMA pipe (the binding one for
+// this recipe, profiles/r02_micro_*) left to the FFMA2s.
+template <class X>
+__device__ __forceinline__ float dot_206_w64(const uint8_t* gp, const X& x, float q, double A, double B,
+                                             uint32_t one) {
+  const uint4 c = lds128(gp);
+  double m44, m38;
+  asm("mov.b64 %0, 0x42B0000000000000;" : "=d"(m44));  // 2^44
+  asm("mov.b64 %0, 0x4250000000000000;" : "=d"(m38));  // 2^38
+  float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int wi = 0; wi < 4; ++wi) {
+    const uint32_t word = wi == 0 ? c.x : wi == 1 ? c.y : wi == 2 ? c.z : c.w;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t hw = prmt(word, 0x3FF00000u, 0x7604u | (uint32_t(b) << 4));
+      const double v = __hiloint2double(int(hw), 0);
+      double t, d1, d2;
+      asm("fma.rm.f64 %0, %1, %2, %3;" : "=d"(t) : "d"(v), "d"(A), "d"(B));
+      asm("add.rm.f64 %0, %1, %2;" : "=d"(d1) : "d"(t), "d"(m44));
+      asm("add.rm.f64 %0, %1, %2;" : "=d"(d2) : "d"(t), "d"(m38));
+      const uint32_t hi = uint32_t(__double2loint(d1)), h2 = uint32_t(__double2loint(d2));
+      const float2 f01 = make_float2(fm<0x007E0000u>(hi, one), fm<0x000FC000u>(hi, one));
+      const float2 f23 = make_float2(fm<0x007E0000u>(h2, one), fm<0x000FC000u>(h2, one));
+      const float4 xx = x.f4(4 * wi + b);
+      if (b & 1) {
+        a1 = __ffma2_rn(f01, make_float2(xx.x, xx.y), a1);
+        a1 = __ffma2_rn(f23, make_float2(xx.z, xx.w), a1);
+      } else {
+        a0 = __ffma2_rn(f01, make_float2(xx.x, xx.y), a0);
+        a0 = __ffma2_rn(f23, make_float2(xx.z, xx.w), a0);
+      }
+    }
+  }
+  return fmaf(64.f, a0.x + a1.x, fmaf(512.f, a0.y + a1.y, -q));
+}
+
 // 2.75: 22 bytes (21 full bytes of 3 states + tail byte: state | scale).
 // Returns the dot and the embedded scale code via *sc.
 template <class X>
@@ -415,14 +456,15 @@ __device__ __forceinline__ void load_x64_smem(const uint8_t* xs, int64_t base, f
 //                [rings: warps][S][SB] | [mbarriers: warps][S]
 // One stage SB = RPW * (CGB codes + 16 nibble bytes + 16 plan bytes).
 // ---------------------------------------------------------------------------
-template <int FAM, int RPW, int MT, int S, int XDT>
+template <int FAM, int RPW, int MT, int S, int XDT, bool W64 = false>
 __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   using T = G64<FAM>;
   constexpr bool XREG = MT == 1;
   constexpr bool SIDE = FAM == kF206;
   constexpr int CGB = (32 * T::PB + 15) & ~15;
   constexpr int REC = CGB + (SIDE ? 32 : 0);  // one (chunk, row) record
-  constexpr int SB = RPW * REC;
+  constexpr int SBR = RPW * REC;                // the tile's records
+  constexpr int SB = SBR + (W64 ? RPW * 16 : 0);  // + the rows' FP64 plans
   extern __shared__ __align__(128) uint8_t smem[];
   const DevLayout& L = a.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -515,8 +557,9 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
       const int64_t r0 = w_begin + int64_t(t) * RPW;
       const uint32_t nr = uint32_t(w_end - r0 < RPW ? w_end - r0 : RPW);
       // codes (+ nibbles + plan) of nr consecutive rows: ONE bulk copy
-      mbar_arrive_expect_tx(&bars[s], nr * REC);
+      mbar_arrive_expect_tx(&bars[s], nr * REC + (W64 ? nr * 16 : 0));
       bulk_g2s_evict_first(ring + s * SB, src + r0 * REC, nr * REC, &bars[s], pol);
+      if constexpr (W64) bulk_g2s(ring + s * SB + SBR, L.plan64 + r0, nr * 16, &bars[s]);
     }
   };
 #pragma unroll
@@ -635,15 +678,17 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
         uint32_t sel[4];
         float sc206 = 0.f;
         if constexpr (SIDE) {
-          const uint4 pv = lds128(st + r * REC + CGB + 16);
-          pl.C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
-          pl.M = pv.z;
-          pl.sel = pv.w;
-          const uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
-          sel[0] = base;
-          sel[1] = base + step;
-          sel[2] = base + 2 * step;
-          sel[3] = base + 3 * step;
+          if constexpr (!W64) {
+            const uint4 pv = lds128(st + r * REC + CGB + 16);
+            pl.C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
+            pl.M = pv.z;
+            pl.sel = pv.w;
+            const uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
+            sel[0] = base;
+            sel[1] = base + step;
+            sel[2] = base + 2 * step;
+            sel[3] = base + 3 * step;
+          }
           const uint8_t nib = st[r * REC + CGB + (lane >> 1)];
           sc206 = float((nib >> (4 * (lane & 1))) & 0xF);
         }
@@ -652,7 +697,11 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
           XGroup<FAM, XREG> xm = xg;
           if constexpr (!XREG) xm.p = xs + m * xstride + int64_t(g) * T::XG;
           float sc, dot;
-          if constexpr (FAM == kF206) {
+          if constexpr (FAM == kF206 && W64) {
+            const double2 p64 = *reinterpret_cast<const double2*>(st + SBR + r * 16);
+            dot = dot_206_w64(gp, xm, qv[m], p64.x, p64.y, one);
+            sc = sc206;
+          } else if constexpr (FAM == kF206) {
             dot = dot_206(gp, xm, qv[m], pl, sel, one);
             sc = sc206;
           } else if constexpr (FAM == kF275) {
@@ -939,13 +988,13 @@ __global__ void __launch_bounds__(256) gemv_generic(GenericArgs a) {
 
 
 
-template <int FAM, int RPW, int MT, int S, int XDT>
+template <int FAM, int RPW, int MT, int S, int XDT, bool W64 = false>
 int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
                   void* y, int y_dtype, cudaStream_t s, const int32_t* offsets = nullptr, int E = 0,
                   int64_t rows_e = 0, int nhit = 0) {
   using T = G64<FAM>;
   constexpr int CGB = (32 * T::PB + 15) & ~15;
-  constexpr int SB = RPW * (CGB + (FAM == kF206 ? 32 : 0));
+  constexpr int SB = RPW * (CGB + (FAM == kF206 ? 32 : 0)) + (W64 ? RPW * 16 : 0);
   if (m->rec != uint32_t(CGB + (FAM == kF206 ? 32 : 0))) return fail(CCQ_ERR_CONFIG, "unexpected device record size");
   GemvArgs a{};
   a.L = layout_of(m);
@@ -990,7 +1039,7 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
     if (smem <= size_t(max_smem)) break;
   }
   if (a.streams < 1) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");
-  auto kern = gemv_stream<FAM, RPW, MT, S, XDT>;
+  auto kern = gemv_stream<FAM, RPW, MT, S, XDT, W64>;
   if (int st = ensure_smem(reinterpret_cast<const void*>(kern), smem)) return st;
   // Programmatic stream serialization: the prologue and the weight copies of
   // this launch overlap the tail of the previous kernel in the stream (the
@@ -1085,6 +1134,18 @@ int launch_res(const ccq_dev_model* m, const void* x, int x_dtype, void* y, int 
 template <int FAM, int RPW, int MT, int S>
 int launch_stream(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M0, int64_t Mn,
                   void* y, int y_dtype, cudaStream_t s) {
+  // measured slower in the full kernel (13.6 vs 13.0 us at 4096 -> 14336,
+  // profiles/r02_gemv_w64.txt): opt-in only
+  static const bool w64_on = std::getenv("CCQ_W64") && std::atoi(std::getenv("CCQ_W64")) == 1;
+  if constexpr (FAM == kF206 && MT == 1) {
+    if (w64_on && m->w64 && m->plan64) {
+      switch (x_dtype) {
+        case CCQ_DTYPE_F32: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_F32, true>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
+        case CCQ_DTYPE_BF16: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_BF16, true>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
+        default: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_F16, true>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
+      }
+    }
+  }
   switch (x_dtype) {
     case CCQ_DTYPE_F32: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_F32>(m, x, x_dtype, M0, Mn, y, y_dtype, s);
     case CCQ_DTYPE_BF16: return launch_stream_dt<FAM, RPW, MT, S, CCQ_DTYPE_BF16>(m, x, x_dtype, M0, Mn, y, y_dtype, s);

@@ -136,6 +136,7 @@ extern "C" int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t
     view.codes = stack->codes + uint64_t(e) * re * stack->rec;  // same chunk stride (rows_pad)
     view.super = stack->super + e * re;
     view.plan = stack->plan ? stack->plan + e * re : nullptr;
+    view.plan64 = stack->plan64 ? stack->plan64 + e * re : nullptr;
     view.num_experts = 0;
     const auto* xe = static_cast<const uint8_t*>(x) + size_t(offsets_host[e]) * stack->cols * xb;
     auto* ye = static_cast<uint8_t*>(y) + size_t(offsets_host[e]) * re * yb;

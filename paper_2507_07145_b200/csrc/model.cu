@@ -133,18 +133,48 @@ __host__ __device__ bool build_widen_plan(float alpha, float beta, WidenPlan* ou
 // One thread per row of the device model (padding rows get the inert plan):
 // plans, invalid-q masks, the first row without a plan and the smallest byte
 // position any plan uses.
+// FP64-pipe widening plan of one row (gemv.cu dot_206_w64): code =
+// low word of add.rm(fma.rm(v, A, B), 2^52) with v = 1 + q 2^-12 (the byte
+// placed in the high word of a double by one PRMT), A = 4096 alpha (exact),
+// B = (beta + 1/2) - A.  Whenever q alpha + beta is exact in double this is
+// floor(q alpha + beta + 1/2) = lround(q alpha + beta); it is verified here
+// with the very instructions the kernel runs, for every valid q.
+__device__ bool build_plan64(float alpha, float beta, const uint32_t inv[8], double2* out) {
+  const double A = 4096.0 * double(alpha);
+  const double B = __dsub_rn(__dadd_rn(double(beta), 0.5), A);
+  *out = make_double2(A, B);
+  if (!isfinite(A) || !isfinite(B)) return false;
+  for (int q = 0; q < 256; ++q) {
+    if ((inv[q >> 5] >> (q & 31)) & 1u) continue;
+    const double v = __hiloint2double(int(0x3FF00000u | (uint32_t(q) << 8)), 0);
+    const double t = __fma_rd(v, A, B);
+    const double d = __dadd_rd(t, 4503599627370496.0);  // 2^52
+    if (long(uint32_t(__double2loint(d))) != ref_widen(q, alpha, beta) || t < 0.0) return false;
+  }
+  return true;
+}
+
 __global__ void build_plans(const float* __restrict__ alpha, const float* __restrict__ beta, int64_t rows,
                             int64_t rp, WidenPlan* __restrict__ plans, uint32_t* __restrict__ invalid,
-                            unsigned long long* __restrict__ fail_row, unsigned int* __restrict__ pos_min) {
+                            unsigned long long* __restrict__ fail_row, unsigned int* __restrict__ pos_min,
+                            double2* __restrict__ plan64, unsigned int* __restrict__ w64_fail) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= rp) return;
   if (r >= rows) {
     plans[r] = WidenPlan{0, 0, plan_sel(0)};
+    plan64[r] = make_double2(0.0, 0.0);
     return;
   }
   WidenPlan p;
   uint32_t inv[8];
-  if (build_widen_plan(alpha[r], beta[r], &p, inv)) {
+  const bool ok = build_widen_plan(alpha[r], beta[r], &p, inv);
+  double2 p64;
+  if (!ok || !build_plan64(alpha[r], beta[r], inv, &p64)) {
+    atomicExch(w64_fail, 1u);
+    p64 = make_double2(0.0, 0.0);
+  }
+  plan64[r] = p64;
+  if (ok) {
     plans[r] = p;
     atomicMin(pos_min, plan_pos(p));
   } else {
@@ -319,7 +349,8 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   const size_t off_codes = 0;
   const size_t off_super = align_up(off_codes + size_t(m->nch) * size_t(rp) * m->rec, 256);
   const size_t off_plan = align_up(off_super + size_t(rp) * 4, 256);
-  const size_t total = align_up(off_plan + (fc.cluster ? size_t(rp) * sizeof(WidenPlan) : 0), 256) + 256;
+  const size_t off_plan64 = align_up(off_plan + (fc.cluster ? size_t(rp) * sizeof(WidenPlan) : 0), 256);
+  const size_t total = align_up(off_plan64 + (fc.cluster ? size_t(rp) * sizeof(double2) : 0), 256) + 256;
 
   int prev = 0;
   cudaGetDevice(&prev);
@@ -334,8 +365,9 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   const size_t s_inv = align_up(s_ab + (fc.cluster ? size_t(rows) * 8 : 0), 256);
   const size_t s_res = align_up(s_inv + (fc.cluster ? size_t(rows) * 32 : 0), 256), s_total = s_res + 256;
   uint8_t* stage = nullptr;
-  // res[0]: first offending byte offset, res[1]: first row without a plan, res[2] (u32): min plan byte position
-  unsigned long long res[3] = {~0ull, ~0ull, 3ull};
+  // res[0]: first offending byte offset, res[1]: first row without a plan, res[2] (u32): min plan byte
+  // position, res[3] (u32): some row has no exact FP64 widening plan
+  unsigned long long res[4] = {~0ull, ~0ull, 3ull, 0ull};
   WidenPlan* dplans = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&m->base, total);
   if (e == cudaSuccess) {
@@ -362,11 +394,15 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
     build_plans<<<unsigned((rp + 127) / 128), 128>>>(
         reinterpret_cast<const float*>(stage + s_ab), reinterpret_cast<const float*>(stage + s_ab) + rows, rows, rp,
         dplans, reinterpret_cast<uint32_t*>(stage + s_inv), reinterpret_cast<unsigned long long*>(stage + s_res) + 1,
-        reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(stage + s_res) + 2));
+        reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(stage + s_res) + 2),
+        reinterpret_cast<double2*>(static_cast<uint8_t*>(m->base) + off_plan64),
+        reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(stage + s_res) + 3));
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpy(res, stage + s_res, sizeof(res), cudaMemcpyDeviceToHost);
     if (res[1] != ~0ull) plan_fail = int64_t(res[1]);
     m->plan_pos_min = int(uint32_t(res[2]));
+    m->plan64 = reinterpret_cast<double2*>(static_cast<uint8_t*>(m->base) + off_plan64);
+    m->w64 = uint32_t(res[3]) == 0u;
   }
   unsigned long long bad = ~0ull;
   if (e == cudaSuccess && m->nch > 0 && rp > 0) {
