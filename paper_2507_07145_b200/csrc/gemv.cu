@@ -165,6 +165,7 @@ struct GemvArgs {
   int64_t x_stride, y_stride;  // elements between token rows
   int streams;                 // row streams per CTA (warps = nch * streams)
   int rows_per_cta_max;
+  int x_direct;                // M = 1: lanes load their group's x from global (no smem pass)
   // grouped experts, one token per hit expert (offsets != nullptr): the model
   // stacks E experts of rows_e rows; CTA b serves hit expert b % nhit (rows
   // split over the CTAs of that expert), reading x row offsets[e] and
@@ -449,6 +450,24 @@ __device__ __forceinline__ void load_x64_smem(const uint8_t* xs, int64_t base, f
   }
 }
 
+template <int FAM, int XDT>
+__device__ __forceinline__ void load_group_x_reg(const void* xin, int64_t g, XGroup<FAM, true>& xg) {
+  using T = G64<FAM>;
+  float xr[64];
+  load_x64<XDT>(xin, g * 64, xr);
+#pragma unroll
+  for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const int p = T::perm(i);
+    float4& f = xg.v[p >> 2];
+    if ((p & 3) == 0) f.x = xr[i];
+    else if ((p & 3) == 1) f.y = xr[i];
+    else if ((p & 3) == 2) f.z = xr[i];
+    else f.w = xr[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The streaming kernel.
 // Shared memory: [partials: rows_per_cta_max][nch][MT] f32
@@ -573,6 +592,28 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   XGroup<FAM, XREG> xg;
   float qv[MT];
   if constexpr (XREG) {
+   if (a.x_direct) {
+    // Each lane loads its own group's 64 activations (L1-cached global loads,
+    // 128 B bf16 / 256 B f32) and converts them in registers: no shared-memory
+    // pass and no block barrier before the loop.
+    if (active && a.M > 0) {
+      load_group_x_reg<FAM, XDT>(xin, g, xg);
+      float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (T::exact_tail(i)) continue;
+        const int p = T::perm(i);
+        const float4 f = xg.v[p >> 2];
+        const float xv = (p & 3) == 0 ? f.x : (p & 3) == 1 ? f.y : (p & 3) == 2 ? f.z : f.w;
+        q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xv, q4[i & 3]);
+      }
+      qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      qv[0] = 0.f;
+    }
+   } else {
     // Cooperative pass straight from global memory (plain loads: they do not
     // queue behind this SM's weight bulk copies in the TMA unit): f32,
     // permuted per family, 16-byte chunks XOR-swizzled by (group & 15) so
@@ -631,6 +672,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
       qv[0] = 0.f;
     }
     TRACE(11);
+   }
   } else {
     for (int64_t e = threadIdx.x; e < int64_t(MT) * gpr * 64; e += blockDim.x) {
       const int m = int(e / (gpr * 64));
@@ -779,24 +821,6 @@ struct ResArgs {
   int S;                  // ring stages per warp
   int rows_per_cta_max;
 };
-
-template <int FAM, int XDT>
-__device__ __forceinline__ void load_group_x_reg(const void* xin, int64_t g, XGroup<FAM, true>& xg) {
-  using T = G64<FAM>;
-  float xr[64];
-  load_x64<XDT>(xin, g * 64, xr);
-#pragma unroll
-  for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int i = 0; i < 64; ++i) {
-    const int p = T::perm(i);
-    float4& f = xg.v[p >> 2];
-    if ((p & 3) == 0) f.x = xr[i];
-    else if ((p & 3) == 1) f.y = xr[i];
-    else if ((p & 3) == 2) f.z = xr[i];
-    else f.w = xr[i];
-  }
-}
 
 template <int FAM, int RPW, int XDT>
 __global__ void __launch_bounds__(256, 2) gemv_res(ResArgs a) {
@@ -1007,6 +1031,11 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   a.M = int(Mn);
   a.x_stride = m->cols;
   a.y_stride = m->rows;
+  // direct per-lane x loads win on K-heavy layers (more chunks: the shared
+  // x pass grows with K), the shared pass on K <= 4096 (profiles/r02_gemv_xdirect.txt)
+  static const int xd = std::getenv("CCQ_X_DIRECT") ? std::atoi(std::getenv("CCQ_X_DIRECT")) : -1;
+  a.x_direct = MT == 1 && (xd == 1 || (xd < 0 && m->nch > 2)) &&
+               (reinterpret_cast<uintptr_t>(x) & (x_dtype == CCQ_DTYPE_F32 ? 15u : 15u)) == 0 && m->cols % 64 == 0;
 
   int dev = 0;
   cudaGetDevice(&dev);
