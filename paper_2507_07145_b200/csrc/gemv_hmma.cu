@@ -73,6 +73,12 @@ __device__ __forceinline__ void hmma(float (&d)[4], uint32_t a0, uint32_t a1, ui
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// ---------------------------------------------------------------------------
+// Family decode: lane t of a row's 64-weight group yields 8 f16x2 A values
+// (16 weights) for the 4 k-steps; unit_wp() gives (weight, p) of each half so
+// the staged B fragments match.  Register j of lane t feeds k-step j/2 as a0
+// (j even) or a2 (j odd).
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t lds32(const void* p) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)));
@@ -84,12 +90,6 @@ __device__ __forceinline__ uint2 lds64(const void* p) {
   return v;
 }
 
-// ---------------------------------------------------------------------------
-// Family decode: lane t of a row's 64-weight group yields 8 f16x2 A values
-// (16 weights) for the 4 k-steps; unit_wp() gives (weight, p) of each half so
-// the staged B fragments match.  Register j of lane t feeds k-step j/2 as a0
-// (j even) or a2 (j odd).
-// ---------------------------------------------------------------------------
 template <int FAM>
 struct HF;
 
@@ -107,7 +107,7 @@ struct HF<kF206> {
     const int slot = 3 - kind;
     return 16 * t + 4 * (2 * pair + half) + slot;
   }
-  __host__ __device__ static constexpr int p(int j) { return (j % 4) & 1 ? 3 : 0; }
+  __host__ __device__ static constexpr int p(int t, int j, int half) { return (j % 4) & 1 ? 3 : 0; }
   __device__ __forceinline__ static void decode(uint32_t w, const uint32_t (&sel)[4], uint64_t C, uint32_t M,
                                                 uint32_t mg, uint32_t (&u)[8]) {
 #pragma unroll
@@ -122,6 +122,63 @@ struct HF<kF206> {
       u[4 * pr + 2] = lop_or(W6, 0x003F003Fu, mg);
       u[4 * pr + 3] = lop_or(W6, 0x01F801F8u, mg);
     }
+  }
+};
+
+// 2.75 / 2.5: the unit order of the tcgen05 GEMM's decoders (unit_wp,
+// ccq_internal.hpp; gemm_sm100.cu decode_gemm_275 / decode_gemm_25) without
+// the scale multiply - the group scale is applied to the accumulator.
+template <>
+struct HF<kF275> {
+  static constexpr int PB = 22, ZP = 8;
+  __host__ __device__ static constexpr int weight(int t, int j, int h) { return unit_wp(kF275, t, j, h).w; }
+  __host__ __device__ static constexpr int p(int t, int j, int h) { return unit_wp(kF275, t, j, h).p; }
+  // lane t: bytes 5t..5t+4 of the group at g (2-byte aligned) and its bytes
+  // 20 / 21 (the extra field, and the scale in byte 21's low nibble)
+  __device__ __forceinline__ static uint32_t decode(const uint8_t* g, int t, uint32_t sel6, uint32_t mk6,
+                                                    uint32_t mg, uint32_t (&u)[8]) {
+    const uint8_t* p = g + 5 * t;
+    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(p) & 3u);
+    const uint8_t* pa = p - mis;
+    const uint32_t W0 = lds32(pa), W1 = lds32(pa + 4);
+    const uint32_t lo = __funnelshift_r(W0, W1, 8u * mis);
+    const uint32_t hi = W1 >> (8u * mis);
+    const uint8_t* q = g + 20;
+    const uint32_t mq = uint32_t(reinterpret_cast<uintptr_t>(q) & 3u);
+    const uint32_t e = lds32(q - mq) >> (8u * mq);  // byte 20 at [0,8), byte 21 at [8,16)
+    const uint32_t p0 = prmt(lo, 0u, 0x1100u), p1 = prmt(lo, 0u, 0x3322u);
+    u[0] = lop_or(p0, 0x000F000Fu, mg);
+    u[1] = lop_or(p0, 0x003C003Cu, mg);
+    u[2] = lop_or(p0, 0x00F000F0u, mg);
+    u[3] = lop_or(p1, 0x000F000Fu, mg);
+    u[4] = lop_or(p1, 0x003C003Cu, mg);
+    u[5] = lop_or(p1, 0x00F000F0u, mg);
+    u[6] = lop_or(prmt(hi, e, sel6), mk6, mg);
+    u[7] = lop_or(prmt(hi, 0u, 0x0000u), 0x000F003Cu, mg);
+    return (e >> 8) & 0xFu;
+  }
+};
+
+template <>
+struct HF<kF25> {
+  static constexpr int PB = 20, ZP = 4;
+  __host__ __device__ static constexpr int weight(int t, int j, int h) { return unit_wp(kF25, t, j, h).w; }
+  __host__ __device__ static constexpr int p(int t, int j, int h) { return unit_wp(kF25, t, j, h).p; }
+  // lane t: stored words 2t, 2t+1 (one 32-bit word) and words 8, 9 (the
+  // extra fields, and the 13-bit scale in word 9)
+  __device__ __forceinline__ static uint32_t decode(const uint8_t* g, int t, uint32_t sel7, uint32_t mk7,
+                                                    uint32_t mg, uint32_t (&u)[8]) {
+    const uint32_t v = lds32(g + 4 * t), w4 = lds32(g + 16);
+    const uint32_t sv = v >> 9;
+    u[0] = lop_or(v, 0x00070007u, mg);
+    u[1] = lop_or(v, 0x001C001Cu, mg);
+    u[2] = lop_or(v, 0x00700070u, mg);
+    u[3] = lop_or(v, 0x01C001C0u, mg);
+    u[4] = lop_or(sv, 0x00070007u, mg);
+    u[5] = lop_or(sv, 0x001C001Cu, mg);
+    u[6] = lop_or(sv, 0x00700070u, mg);
+    u[7] = lop_or(prmt(w4, w4, sel7), mk7, mg);
+    return (w4 >> 16) & 0x1FFFu;
   }
 };
 
@@ -247,32 +304,79 @@ __global__ void __launch_bounds__(1024, 1) gemv_hmma(HmmaArgs a) {
   HTRACE(2);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int t4 = it & 3, g = (it >> 2) % a.gpr_pad, m = (it >> 2) / a.gpr_pad;
-    uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
-    const bool ok = load16(it, v0, v1);
+    const bool ok = m < a.M && int64_t(g) * 64 < L.cols;
     const float sig = ok ? sigma_of(smax[m]) : 0.f;
-    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    float xv[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if constexpr (XDT == CCQ_DTYPE_BF16) {
-        xv[2 * i] = __uint_as_float(w[i] << 16);
-        xv[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-      } else {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
-        xv[2 * i] = f.x;
-        xv[2 * i + 1] = f.y;
-      }
-    }
     uint32_t r[8];
     float q = 0.f;
+    const uint4* px = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(a.x) + (ok ? m * a.x_stride : 0) +
+                                                     (ok ? int64_t(g) * 64 : 0));
+    if constexpr (FAM == kF206) {
+      // lane t's 16 weights are 16t .. 16t+15 for every t: uniform code
+      float xv[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float sj = sig * (F::p(j) ? 0.125f : 1.f);
-      const __half2 h = __floats2half2_rn(xv[F::weight(0, j, 0)] * sj, xv[F::weight(0, j, 1)] * sj);
-      r[j] = *reinterpret_cast<const uint32_t*>(&h);
-      const float2 b = __half22float2(h);
-      const float cq = 1024.f + float(F::ZP) * float(1 << F::p(j));
-      q = fmaf(cq, b.x, fmaf(cq, b.y, q));
+      for (int i = 0; i < 2; ++i) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ok) v = __ldg(px + 2 * t4 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if constexpr (XDT == CCQ_DTYPE_BF16) {
+            xv[8 * i + 2 * k] = __uint_as_float(w[k] << 16);
+            xv[8 * i + 2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+          } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+            xv[8 * i + 2 * k] = f.x;
+            xv[8 * i + 2 * k + 1] = f.y;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int p0 = F::p(0, j, 0), p1 = F::p(0, j, 1);
+        const __half2 h = __floats2half2_rn(xv[F::weight(0, j, 0)] * sig * (1.f / float(1 << p0)),
+                                            xv[F::weight(0, j, 1)] * sig * (1.f / float(1 << p1)));
+        r[j] = *reinterpret_cast<const uint32_t*>(&h);
+        const float2 b = __half22float2(h);
+        q = fmaf(1024.f + float(F::ZP) * float(1 << p0), b.x, fmaf(1024.f + float(F::ZP) * float(1 << p1), b.y, q));
+      }
+    } else {
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt) {
+      if (tt != t4) continue;
+      // only the 16-byte pieces of the group holding lane tt's 16 weights
+      float xv[64];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        bool need = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          for (int h = 0; h < 2; ++h) need |= F::weight(tt, j, h) / 8 == i;
+        if (!need) continue;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ok) v = __ldg(px + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if constexpr (XDT == CCQ_DTYPE_BF16) {
+            xv[8 * i + 2 * k] = __uint_as_float(w[k] << 16);
+            xv[8 * i + 2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+          } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+            xv[8 * i + 2 * k] = f.x;
+            xv[8 * i + 2 * k + 1] = f.y;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int p0 = F::p(tt, j, 0), p1 = F::p(tt, j, 1);
+        const __half2 h = __floats2half2_rn(xv[F::weight(tt, j, 0)] * sig * (1.f / float(1 << p0)),
+                                            xv[F::weight(tt, j, 1)] * sig * (1.f / float(1 << p1)));
+        r[j] = *reinterpret_cast<const uint32_t*>(&h);
+        const float2 b = __half22float2(h);
+        q = fmaf(1024.f + float(F::ZP) * float(1 << p0), b.x, fmaf(1024.f + float(F::ZP) * float(1 << p1), b.y, q));
+      }
+    }
     }
     uint4* dst = reinterpret_cast<uint4*>(xf + ((size_t(m) * a.gpr_pad + g) * 4 + t4) * 8);
     dst[0] = make_uint4(r[0], r[1], r[2], r[3]);
@@ -292,6 +396,17 @@ __global__ void __launch_bounds__(1024, 1) gemv_hmma(HmmaArgs a) {
   const int tok = MT == 1 ? 0 : (g8 < a.M ? g8 : 0);  // B column of this lane
   uint32_t mg;
   asm volatile("mov.b32 %0, 0x64006400;" : "=r"(mg));
+  // lane-dependent selector / mask of the last unit (2.75: unit 6, 2.5: unit 7)
+  uint32_t xsel = 0, xmk = 0;
+  if constexpr (FAM == kF275) {
+    const uint32_t eb = 4u + (t == 3 ? 1u : 0u);
+    const uint32_t me = t == 0 ? 0xF0u : t == 1 ? 0x3Cu : t == 2 ? 0x0Fu : 0xF0u;
+    xsel = (eb << 12) | (eb << 8);
+    xmk = 0x000000F0u | (me << 16);
+  } else if constexpr (FAM == kF25) {
+    xsel = t == 0 ? 0x1010u : t == 1 ? 0x1010u : t == 2 ? 0x1111u : 0x3311u;
+    xmk = t == 0 ? 0x001C0007u : t == 1 ? 0x01C00070u : t == 2 ? 0x0038000Eu : 0x00E000E0u;
+  }
   const int nitems = nunits * kSlices;
 #pragma unroll 1
   for (int i = warp; i < nitems; i += nw) {
@@ -320,15 +435,17 @@ __global__ void __launch_bounds__(1024, 1) gemv_hmma(HmmaArgs a) {
         sel1[b] = (p1.w & 0xFFFFu) + uint32_t(b) * (p1.w >> 16);
       }
     }
-    const uint32_t nib0 = lds32(r0 + CGB + 4 * sl), nib1 = lds32(r1 + CGB + 4 * sl);
+    uint32_t nib0 = 0, nib1 = 0;
+    if constexpr (FAM == kF206) {
+      nib0 = lds32(r0 + CGB + 4 * sl);
+      nib1 = lds32(r1 + CGB + 4 * sl);
+    }
     float yacc[4] = {0.f, 0.f, 0.f, 0.f};
     const int gbase = c * kChunk + sl * kGroupsPerSlice;
 #pragma unroll 2
     for (int gi = 0; gi < kGroupsPerSlice; ++gi) {
       const int gl = sl * kGroupsPerSlice + gi;  // group within the chunk
       const int g = gbase + gi;
-      const uint32_t w0 = lds32(r0 + gl * F::PB + 4 * t);
-      const uint32_t w1 = lds32(r1 + gl * F::PB + 4 * t);
       const uint4 b01 = lds128(xf + ((size_t(tok) * a.gpr_pad + g) * 4 + t) * 8);
       const uint4 b23 = lds128(xf + ((size_t(tok) * a.gpr_pad + g) * 4 + t) * 8 + 4);
       float d[4];
@@ -345,8 +462,18 @@ __global__ void __launch_bounds__(1024, 1) gemv_hmma(HmmaArgs a) {
         d[1] = d[3] = __uint_as_float(qq.y);
       }
       uint32_t u0[8], u1[8];
-      F::decode(w0, sel0, C0, M0, mg, u0);
-      F::decode(w1, sel1, C1, M1, mg, u1);
+      float sc0, sc1;
+      if constexpr (FAM == kF206) {
+        const uint32_t w0 = lds32(r0 + gl * F::PB + 4 * t);
+        const uint32_t w1 = lds32(r1 + gl * F::PB + 4 * t);
+        F::decode(w0, sel0, C0, M0, mg, u0);
+        F::decode(w1, sel1, C1, M1, mg, u1);
+        sc0 = float((nib0 >> (4 * gi)) & 0xFu);
+        sc1 = float((nib1 >> (4 * gi)) & 0xFu);
+      } else {
+        sc0 = float(F::decode(r0 + gl * F::PB, t, xsel, xmk, mg, u0));
+        sc1 = float(F::decode(r1 + gl * F::PB, t, xsel, xmk, mg, u1));
+      }
       // two independent accumulator chains (k-steps 0,1 and 2,3)
       float e[4] = {0.f, 0.f, 0.f, 0.f};
       hmma(d, u0[0], u1[0], u0[1], u1[1], b01.x, b01.y);
@@ -359,7 +486,6 @@ __global__ void __launch_bounds__(1024, 1) gemv_hmma(HmmaArgs a) {
         d[1] += e[1];
         d[3] += e[3];
       }
-      const float sc0 = float((nib0 >> (4 * gi)) & 0xFu), sc1 = float((nib1 >> (4 * gi)) & 0xFu);
       yacc[0] = fmaf(sc0, d[0], yacc[0]);
       yacc[2] = fmaf(sc1, d[2], yacc[2]);
       if constexpr (MT > 1) {
@@ -509,7 +635,10 @@ int launch_xdt(const ccq_dev_model* m, const void* x, int64_t M, void* y, int y_
 bool gemv_hmma_supported(const ccq_dev_model* m, int64_t M, int x_dtype, const void* x) {
   static const int mode = std::getenv("CCQ_GEMV_HMMA") ? std::atoi(std::getenv("CCQ_GEMV_HMMA")) : 1;
   if (mode == 0 || (mode == 1 && M == 1)) return false;  // 2: also M = 1
-  if (m->family != kF206 || m->geo.group_size != 64 || !m->fast) return false;
+  if (m->geo.group_size != 64 || !m->fast) return false;
+  // 2.75 / 2.5 decode as fast on r01's gemv_mma (profiles/r02_gemv_hmma_families.txt): 2.06 only by default
+  static const int fams = std::getenv("CCQ_HMMA_FAMS") ? std::atoi(std::getenv("CCQ_HMMA_FAMS")) : (1 << kF206);
+  if (!((fams >> m->family) & 1)) return false;
   if (x_dtype != CCQ_DTYPE_BF16 && x_dtype != CCQ_DTYPE_F16) return false;
   // activations are staged with 16-byte loads of whole 64-weight groups
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0 || m->cols % 64 != 0) return false;
@@ -518,10 +647,15 @@ bool gemv_hmma_supported(const ccq_dev_model* m, int64_t M, int x_dtype, const v
 
 int launch_gemv_hmma(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                      cudaStream_t s) {
-  int st;
-  if (x_dtype == CCQ_DTYPE_BF16) st = launch_xdt<kF206, CCQ_DTYPE_BF16>(m, x, M, y, y_dtype, s);
-  else st = launch_xdt<kF206, CCQ_DTYPE_F16>(m, x, M, y, y_dtype, s);
-  return st;
+  const bool bf = x_dtype == CCQ_DTYPE_BF16;
+  switch (m->family) {
+    case kF275: return bf ? launch_xdt<kF275, CCQ_DTYPE_BF16>(m, x, M, y, y_dtype, s)
+                          : launch_xdt<kF275, CCQ_DTYPE_F16>(m, x, M, y, y_dtype, s);
+    case kF25: return bf ? launch_xdt<kF25, CCQ_DTYPE_BF16>(m, x, M, y, y_dtype, s)
+                         : launch_xdt<kF25, CCQ_DTYPE_F16>(m, x, M, y, y_dtype, s);
+    default: return bf ? launch_xdt<kF206, CCQ_DTYPE_BF16>(m, x, M, y, y_dtype, s)
+                       : launch_xdt<kF206, CCQ_DTYPE_F16>(m, x, M, y, y_dtype, s);
+  }
 }
 
 }  // namespace ccqb
