@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "ccq_internal.hpp"
 
 namespace ccqb {
@@ -162,18 +164,20 @@ __global__ void build_plans(const float* __restrict__ alpha, const float* __rest
   if (r >= rp) return;
   if (r >= rows) {
     plans[r] = WidenPlan{0, 0, plan_sel(0)};
-    plan64[r] = make_double2(0.0, 0.0);
+    if (plan64) plan64[r] = make_double2(0.0, 0.0);
     return;
   }
   WidenPlan p;
   uint32_t inv[8];
   const bool ok = build_widen_plan(alpha[r], beta[r], &p, inv);
-  double2 p64;
-  if (!ok || !build_plan64(alpha[r], beta[r], inv, &p64)) {
-    atomicExch(w64_fail, 1u);
-    p64 = make_double2(0.0, 0.0);
+  if (plan64) {  // only when the FP64-widening GEMV is enabled (CCQ_W64=1)
+    double2 p64;
+    if (!ok || !build_plan64(alpha[r], beta[r], inv, &p64)) {
+      atomicExch(w64_fail, 1u);
+      p64 = make_double2(0.0, 0.0);
+    }
+    plan64[r] = p64;
   }
-  plan64[r] = p64;
   if (ok) {
     plans[r] = p;
     atomicMin(pos_min, plan_pos(p));
@@ -349,8 +353,10 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
   const size_t off_codes = 0;
   const size_t off_super = align_up(off_codes + size_t(m->nch) * size_t(rp) * m->rec, 256);
   const size_t off_plan = align_up(off_super + size_t(rp) * 4, 256);
+  static const bool want_w64_env = std::getenv("CCQ_W64") && std::atoi(std::getenv("CCQ_W64")) == 1;
+  const bool want_w64 = fc.cluster && want_w64_env;
   const size_t off_plan64 = align_up(off_plan + (fc.cluster ? size_t(rp) * sizeof(WidenPlan) : 0), 256);
-  const size_t total = align_up(off_plan64 + (fc.cluster ? size_t(rp) * sizeof(double2) : 0), 256) + 256;
+  const size_t total = align_up(off_plan64 + (want_w64 ? size_t(rp) * sizeof(double2) : 0), 256) + 256;
 
   int prev = 0;
   cudaGetDevice(&prev);
@@ -395,14 +401,16 @@ int ccq_cuda_model_upload_rows(const ccq_packed_view* v, int64_t r0, int64_t r1,
         reinterpret_cast<const float*>(stage + s_ab), reinterpret_cast<const float*>(stage + s_ab) + rows, rows, rp,
         dplans, reinterpret_cast<uint32_t*>(stage + s_inv), reinterpret_cast<unsigned long long*>(stage + s_res) + 1,
         reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(stage + s_res) + 2),
-        reinterpret_cast<double2*>(static_cast<uint8_t*>(m->base) + off_plan64),
+        want_w64 ? reinterpret_cast<double2*>(static_cast<uint8_t*>(m->base) + off_plan64) : nullptr,
         reinterpret_cast<unsigned int*>(reinterpret_cast<unsigned long long*>(stage + s_res) + 3));
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpy(res, stage + s_res, sizeof(res), cudaMemcpyDeviceToHost);
     if (res[1] != ~0ull) plan_fail = int64_t(res[1]);
     m->plan_pos_min = int(uint32_t(res[2]));
-    m->plan64 = reinterpret_cast<double2*>(static_cast<uint8_t*>(m->base) + off_plan64);
-    m->w64 = uint32_t(res[3]) == 0u;
+    if (want_w64) {
+      m->plan64 = reinterpret_cast<double2*>(static_cast<uint8_t*>(m->base) + off_plan64);
+      m->w64 = uint32_t(res[3]) == 0u;
+    }
   }
   unsigned long long bad = ~0ull;
   if (e == cudaSuccess && m->nch > 0 && rp > 0) {
