@@ -239,6 +239,11 @@ struct GemmArgs {
   // (device-computed, so the launch needs no host copy of the routing)
   const int32_t* tile_prefix;
   int E;
+  // dense L2-aware raster (raster_group > 0): a 1-D grid of nt x nr tiles
+  // walked as groups of raster_group row tiles, row tile fastest, so one wave
+  // of CTAs covers few token tiles (activation tiles, the big operand) and
+  // many row tiles: activations are read ~(nr / group) times, not ~(nr / wave_rows)
+  int raster_group, raster_nt, raster_nr;
 };
 
 __device__ __forceinline__ uint32_t lop_mask_or(uint32_t v, uint32_t mask, uint32_t magic) {
@@ -495,9 +500,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     y_ld = a.rows_e;
     y_col0 = e * a.rows_e;
   } else {
-    r0 = int64_t(blockIdx.y) * kBM;
+    int bt = int(blockIdx.x), br = int(blockIdx.y);
+    if (a.raster_group > 0) {
+      const int pid = int(blockIdx.x), per_group = a.raster_group * a.raster_nt;
+      const int gid = pid / per_group, first = gid * a.raster_group;
+      const int gsz = min(a.raster_nr - first, a.raster_group);
+      br = first + (pid % per_group) % gsz;
+      bt = (pid % per_group) / gsz;
+    }
+    r0 = int64_t(br) * kBM;
     row_end = a.rows < r0 + kBM ? a.rows : r0 + kBM;
-    n0 = blockIdx.x * tb;
+    n0 = bt * tb;
     tok_end = a.M;
     y_ld = a.rows;
     y_col0 = 0;
@@ -899,7 +912,7 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
   }
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
              offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr,
-             tile_prefix, E};
+             tile_prefix, E, 0, 0, 0};
   auto kern = gemm_ccq<FAM, BN>;
   if (int st2 = ensure_smem(reinterpret_cast<const void*>(kern), SM::TOTAL)) {
     cudaFreeAsync(x16, s);
@@ -934,6 +947,22 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
       } else {
         splits = 1;
       }
+    }
+  }
+  // L2-aware raster for multi-wave dense grids: a wave of `sms` CTAs covers
+  // ~sms / group token tiles x group row tiles (profiles/r02_gemm_raster.txt)
+  static const int raster_env = std::getenv("CCQ_GEMM_RASTER") ? std::atoi(std::getenv("CCQ_GEMM_RASTER")) : -1;
+  if (!grouped && splits == 1 && grid.x > 1 && raster_env != 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int64_t sms = num_sms(dev);
+    const int64_t nt = grid.x, nr = grid.y;
+    if (nt * nr > sms) {
+      int gsz = raster_env > 0 ? raster_env : int(std::max<int64_t>(1, sms / std::min<int64_t>(nt, 4)));
+      a.raster_group = int(std::min<int64_t>(gsz, nr));
+      a.raster_nt = int(nt);
+      a.raster_nr = int(nr);
+      grid = dim3(unsigned(nt * nr), 1, 1);
     }
   }
   if (grid.x && grid.y) {
