@@ -313,6 +313,8 @@ def gemv(model, x, y=None) -> np.ndarray:
     d = _dev(model)
     x = np.ascontiguousarray(x, np.float32).reshape(-1)
     out = np.empty(d.rows, np.float32) if y is None else y
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous):
+        raise ShapeError("y must be a C-contiguous float32 array")
     _check(lib().ccq_gemv_host(d.h, _np_ptr(x), x.size, _np_ptr(out), out.size))
     return out
 
@@ -324,6 +326,8 @@ def gemv_batch(model, x, y=None) -> np.ndarray:
     if x.ndim != 2:
         raise ShapeError("gemv_batch expects a 2-D activation matrix")
     out = np.empty((x.shape[0], d.rows), np.float32) if y is None else y
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous and out.ndim == 2):
+        raise ShapeError("y must be a C-contiguous 2-D float32 array")
     _check(lib().ccq_gemv_batch_host(d.h, _np_ptr(x), x.shape[0], x.shape[1], _np_ptr(out),
                                      out.shape[0], out.shape[1]))
     return out
@@ -388,9 +392,14 @@ def matmul(model: DeviceModel, x, out=None, kernel: str = "auto", out_dtype=None
         raise ShapeError("activations must be contiguous")
     if x.shape[1] != model.cols:
         raise ShapeError("activation width does not match the model")
+    if not x.is_cuda:
+        raise ShapeError("activations must be a CUDA tensor")
     if out is None:
         out = torch.empty(x.shape[0], model.rows, dtype=out_dtype or torch.float32,
                           device=x.device)
+    elif (tuple(out.shape) != (x.shape[0], model.rows) or out.dtype not in (torch.float32, torch.bfloat16)
+          or not out.is_contiguous() or out.device != x.device):
+        raise ShapeError("out must be a contiguous float32/bfloat16 [M, rows] tensor on the activations' device")
     L = lib()
     fn = L.ccq_cuda_matmul if kernel == "auto" else {"gemv": L.ccq_cuda_gemv, "gemm": L.ccq_cuda_gemm}[kernel]
     _check(fn(model.h, x.data_ptr(), _torch_dtype_code(x), x.shape[0], out.data_ptr(),

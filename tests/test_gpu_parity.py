@@ -785,3 +785,22 @@ def test_config0_full_size_gaussian_quantized(oracle, ccq, cuda):
         dt = torch.bfloat16 if xin is not x else torch.float32
         y = ccq.matmul(d, torch.from_numpy(xin).to("cuda").to(dt)).cpu().numpy()
         assert rel_err(y, want) < 1e-4
+
+
+def test_matmul_rejects_bad_output_buffers(oracle, ccq, cuda):
+    """out= must be a contiguous f32/bf16 [M, rows] tensor on the activations'
+    device; host gemv outputs must be C-contiguous float32 (no silent overrun)."""
+    torch = cuda
+    s = oracle.random_packed(32, 128, 2, 64, seed=3)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = torch.randn(2, 128, device="cuda").to(torch.bfloat16)
+    for bad in (torch.empty(2, 32, dtype=torch.float16, device="cuda"), torch.empty(2, 16, device="cuda"),
+                torch.empty(32, 2, device="cuda").t(), torch.empty(2, 32)):
+        with pytest.raises(ccq.ShapeError):
+            ccq.matmul(d, x, out=bad)
+    with pytest.raises(ccq.ShapeError):
+        ccq.matmul(d, x.cpu())
+    with pytest.raises(ccq.ShapeError):
+        ccq.gemv(d, np.zeros(128, np.float32), np.zeros(32, np.float64))
+    with pytest.raises(ccq.ShapeError):
+        ccq.gemv_batch(d, np.zeros((2, 128), np.float32), np.zeros((32, 2), np.float32).T)
