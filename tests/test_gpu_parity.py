@@ -804,3 +804,30 @@ def test_matmul_rejects_bad_output_buffers(oracle, ccq, cuda):
         ccq.gemv(d, np.zeros(128, np.float32), np.zeros(32, np.float64))
     with pytest.raises(ccq.ShapeError):
         ccq.gemv_batch(d, np.zeros((2, 128), np.float32), np.zeros((32, 2), np.float32).T)
+
+
+def test_fp64_widening_variant_subprocess(cuda):
+    """The opt-in FP64-pipe widening (CCQ_W64=1: plans built and verified at
+    upload, gemv_stream's dot_206_w64) gives the same M = 1 products as the
+    default IMAD.WIDE plan path (bit for bit: same fields, same float ops)."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import oracle as O, paper_2507_07145_b200 as P\n"
+        "s = O.random_packed(300, 4096, 2, 64, seed=5)\n"
+        "d = P.DeviceModel.upload(P.PackedModel.from_sections(s))\n"
+        "x = torch.from_numpy(O.random_matrix(1, 4096, 'gaussian', 3)).cuda().to(torch.bfloat16)\n"
+        "y = P.matmul(d, x).cpu().numpy()\n"
+        "np.save(sys.argv[1], y)\n" % ROOT)
+    outs = []
+    for w64, name in (("1", "a.npy"), ("0", "b.npy")):
+        import os
+        import tempfile
+        path = os.path.join(tempfile.mkdtemp(), name)
+        r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, CCQ_W64=w64),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))

@@ -26,6 +26,15 @@ for fam in (2, 0, 1):
     P.experts_matmul(ex, offs, torch.from_numpy(O.random_matrix(4, 1088, "gaussian", 9)).cuda().to(torch.bfloat16))
     offs1 = np.array([0, 1, 1, 2, 3], np.int32)  # one token per routed expert: grouped streaming GEMV
     P.experts_matmul(ex, offs1, torch.from_numpy(O.random_matrix(3, 1088, "gaussian", 10)).cuda().to(torch.bfloat16))
+    # sync-free MoE forward (token-tile prefix + tile-list grouped GEMM + combine)
+    ids = torch.tensor([[0, 2], [3, 1], [2, 0]], dtype=torch.int32, device="cuda")
+    P.moe_forward(ex, ids, torch.rand(3, 2, device="cuda"),
+                  torch.from_numpy(O.random_matrix(3, 1088, "gaussian", 11)).cuda().to(torch.bfloat16))
+    # K-heavy layer (> 2 K chunks): direct activation loads in the M = 1 GEMV; M = 8 tensor-pipe GEMV
+    sk = O.random_packed(64, 64 * 96, fam, 64, seed=21 + fam)
+    dk = P.DeviceModel.upload(P.PackedModel.from_sections(sk))
+    for M in (1, 8):
+        P.matmul(dk, torch.from_numpy(O.random_matrix(M, 64 * 96, "gaussian", M)).cuda().to(torch.bfloat16))
     # quantizer kernels (csrc/quantize.cu)
     wq = (np.random.default_rng(fam).standard_normal((4, 128)) * 0.02).astype(np.float32)
     P.quantize(wq, fam, 64, 1)
