@@ -712,9 +712,13 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     if (t == 0) { TRACE(2); }
     ++ntiles_done;
     const uint8_t* st = ring + s * SB;
+    // rows of this tile (the last tile of a stream may be short): rows past
+    // it hold a previous tile's bytes and are skipped, not decoded
+    const int nr = int(w_end - r0 < RPW ? w_end - r0 : RPW);
     if (active) {
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
+        if (r > 0 && r >= nr) break;
         const uint8_t* gp = st + r * REC + lane * T::PB;
         WidenPlan pl;
         uint32_t sel[4];
@@ -900,9 +904,11 @@ __global__ void __launch_bounds__(256, 2) gemv_res(ResArgs a) {
     for (int i = 0; i < RPW; ++i) acc[i] = 0.f;
     mbar_wait(&bars[s], uint32_t((t / S) & 1));
     const uint8_t* st = ring + size_t(s) * SB;
+    const int nr = int(w_end - r0 < RPW ? w_end - r0 : RPW);
     if (active) {
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
+        if (r > 0 && r >= nr) break;
         const uint8_t* gp = st + r * REC + lane * T::PB;
         float sc, dot;
         if constexpr (FAM == kF206) {

@@ -1,7 +1,7 @@
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "decode or loader or acceptance or zero_scale or empty or config0" > $OUT/pytest_dec.log 2>&1; echo "rc=$?" >> $OUT/pytest_dec.log
-timeout 300 python tools/time_decode.py > $OUT/decode_time.txt 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:decode_rec -s 4 -c 1 -o $OUT/prof_decode -f python tools/prof_kernel.py --family 2.06 --din 4096 --dout 14336 --decode > $OUT/ncu_decode.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gemv or baseline or randomized or experts or config0" > $OUT/pytest_skip.log 2>&1; echo "rc=$?" >> $OUT/pytest_skip.log
+for f in 2.06 2.75 2.5; do timeout 600 python tools/time_matmul.py --family $f --shapes 4096x14336,14336x4096,4096x4096,8192x28672 --M 1 >> $OUT/skip_t.txt 2>&1; done
+timeout 300 python tools/trace_gemv.py 2.06 4096 14336 > $OUT/trace_gemv_r02b.txt 2>&1
 echo done
