@@ -200,14 +200,19 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
 
     # --- synthetic layers: L resident copies (different seeds) -------------
-    from paper_2507_07145_b200.synthetic import random_packed as _synthetic
+    # The reference bench generator itself (random_quantized + pack_model,
+    # mt19937_64, ccq_synthetic_packed): layer 0 of rank 0 is byte-identical
+    # to the model the reference arm times (RefModel.random(..., SEED)), and
+    # the activations are the reference's random_matrix(M, d_in, Gaussian,
+    # SEED + 1) rounded to bf16 (ccq_synthetic_matrix).
+    from paper_2507_07145_b200.synthetic import reference_matrix, reference_packed
     layers = []
     for l in range(args.layers):
-        s = _synthetic(D_OUT, D_IN, FAMILY, 64, SEED + 1000 * l + rank)
+        s = reference_packed(D_OUT, D_IN, FAMILY, 64, SEED + 1000 * l + rank)
         layers.append(P.DeviceModel.upload(s, device=local))
     payload = layers[0].payload_bytes
-    gen = torch.Generator(device="cpu").manual_seed(SEED + rank)
-    x_host = torch.randn(args.layers, M_HEAD, D_IN, generator=gen).to(torch.bfloat16).pin_memory()
+    x_host = torch.from_numpy(np.stack([reference_matrix(M_HEAD, D_IN, "gaussian", SEED + 1 + 1000 * l + rank)
+                                        for l in range(args.layers)])).to(torch.bfloat16).pin_memory()
     x_dev = x_host.to(dev)
     y_dev = torch.empty(args.layers, M_HEAD, D_OUT, dtype=torch.float32, device=dev)
     y_host = torch.empty_like(y_dev, device="cpu").pin_memory()
@@ -360,8 +365,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16 activations x CCQ codes, f32 accumulate",
-            "data": "synthetic: random_quantized CCQ 2.06 weights (synthetic.cpp:25-103), "
-                    "Gaussian bf16 activations",
+            "data": "synthetic: the reference generator's bytes (random_quantized + pack_model, "
+                    "synthetic.cpp:25-103, mt19937_64; layer 0 = the reference arm's model), "
+                    "random_matrix Gaussian activations rounded to bf16",
             "config": base_config(args.layers),
             "arm": f"B200 kernels, replicas x{world}",
             "l2": f"inputs larger than L2: {args.layers} resident layer copies = "

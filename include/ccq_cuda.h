@@ -202,6 +202,22 @@ int ccq_cuda_shard_allgather(const ccq_dev_model* shard, int64_t rows_total, int
                              const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                              int64_t chunk_tokens, void* comm, void* stream);
 
+/* ---- synthetic models (bench harness) ---- */
+
+/* pack_model(random_quantized(rows, cols, family, group_size, seed)) of the
+ * reference bench generator (synthetic.cpp:25-103, container.cpp:323-358),
+ * draw for draw (std::mt19937_64): the reference's exact bytes for a seed.
+ * Host only (no device).  Buffers: code_payload rows*(cols/g)*payload_bytes,
+ * scale_payload (groups+1)/2 (side-band families), super_scales rows,
+ * cluster_scales / cluster_zero_points rows (2.06). */
+int ccq_synthetic_packed(int64_t rows, int64_t cols, int32_t family, int32_t group_size, uint64_t seed,
+                         uint8_t* code_payload, uint8_t* scale_payload, float* super_scales,
+                         float* cluster_scales, float* cluster_zero_points);
+
+/* random_matrix (tensor.cpp:37-69), the reference's generator draw for draw:
+ * dist 0 = Gaussian, 1 = uniform [-1, 1).  out: rows*cols f32, row-major. */
+int ccq_synthetic_matrix(int64_t rows, int64_t cols, int32_t dist, uint64_t seed, float* out);
+
 /* ---- synchronous host-buffer entry points (the reference signatures) ---- */
 
 /* ccq::dequantize (kernels.hpp:36). out: host rows x cols f32. */

@@ -104,7 +104,7 @@ ABI_SYMBOLS = [
     "ccq_clustered_code_value", "ccq_cuda_launch_count", "ccq_cuda_experts_upload",
     "ccq_cuda_experts_matmul", "ccq_cuda_moe_forward", "ccq_cuda_search_codes",
     "ccq_quantize_host", "ccq_cuda_quantize_model", "ccq_nccl_unique_id", "ccq_nccl_comm_init",
-    "ccq_nccl_comm_destroy", "ccq_cuda_shard_allgather",
+    "ccq_nccl_comm_destroy", "ccq_cuda_shard_allgather", "ccq_synthetic_packed", "ccq_synthetic_matrix",
 ]
 
 _lib = None
@@ -141,6 +141,8 @@ def lib():
         L.ccq_cuda_search_codes.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i32, vp, vp]
         L.ccq_quantize_host.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.ccq_cuda_quantize_model.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp]
+        L.ccq_synthetic_packed.argtypes = [i64, i64, i32, i32, u64, vp, vp, vp, vp, vp]
+        L.ccq_synthetic_matrix.argtypes = [i64, i64, i32, u64, vp]
         L.ccq_nccl_unique_id.argtypes = [vp]
         L.ccq_nccl_comm_init.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.ccq_nccl_comm_destroy.argtypes = [vp]

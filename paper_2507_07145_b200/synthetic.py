@@ -1,12 +1,16 @@
-"""Synthetic packed models for benchmarks (numpy, vectorised).
+"""Synthetic packed models for benchmarks.
 
-Same distribution as the reference bench generator random_quantized
-(synthetic.cpp:25-103, used by `ccq bench`, ccq_main.cpp:269-271): uniform
-stored code words, uniform scale codes in [0, 2^scale_bits), super scales
-~ U[0.001, 0.051), and for the clustered family alpha ~ U[1, 1+32767/512),
-beta ~ U[0, 32767 - 255 alpha).  The random stream is numpy's, not
-mt19937_64, so values differ from the reference's for a given seed; parity
-tests use the oracle's bit-exact restatement instead.
+`reference_packed` is the reference bench generator itself
+(pack_model(random_quantized(...)), synthetic.cpp:25-103, the same
+std::mt19937_64 stream; C++ in libccq_b200.so, ccq_synthetic_packed): a seed
+gives the reference's exact bytes, so the GPU arm and the reference CPU arm
+of bench.py time identical weights.
+
+`random_packed` (numpy, vectorised, faster for big sweeps) draws the same
+distribution - uniform stored code words, uniform scale codes in
+[0, 2^scale_bits), super scales ~ U[0.001, 0.051), and for the clustered
+family alpha ~ U[1, 1+32767/512), beta ~ U[0, 32767 - 255 alpha) - from
+numpy's stream, so its bytes differ from the reference's for a seed.
 """
 from __future__ import annotations
 
@@ -60,6 +64,33 @@ def random_packed(rows: int, cols: int, family: int, group_size: int = 64,
         codes[:, 1::2] = (words >> 8).astype(np.uint8)
         scale = np.zeros(0, np.uint8)
     return PackedModel(rows, cols, family, group_size, codes.reshape(-1), scale, sup, cs, czp)
+
+
+def reference_packed(rows: int, cols: int, family: int, group_size: int = 64, seed: int = 0) -> PackedModel:
+    """The reference's random_quantized + pack_model bytes for `seed`."""
+    from . import _check, _np_ptr, lib
+    g = group_geometry(family, group_size)
+    if cols % group_size:
+        raise ValueError("cols must be a whole number of groups")
+    groups = rows * (cols // group_size)
+    code = np.empty(groups * g["payload_bytes"], np.uint8)
+    scale = np.zeros(0 if g["embedded_scale"] else (groups + 1) // 2, np.uint8)
+    sup = np.empty(rows, np.float32)
+    cs = np.empty(rows if family == 2 else 0, np.float32)
+    czp = np.empty(rows if family == 2 else 0, np.float32)
+    _check(lib().ccq_synthetic_packed(rows, cols, family, group_size, seed, _np_ptr(code),
+                                      _np_ptr(scale) if scale.size else None, _np_ptr(sup),
+                                      _np_ptr(cs) if cs.size else None, _np_ptr(czp) if czp.size else None))
+    return PackedModel(rows, cols, family, group_size, code, scale, sup, cs, czp)
+
+
+def reference_matrix(rows: int, cols: int, dist: str = "gaussian", seed: int = 0) -> np.ndarray:
+    """The reference's random_matrix (tensor.cpp:37-69) for `seed`, f32."""
+    from . import _check, _np_ptr, lib
+    out = np.empty((rows, cols), np.float32)
+    _check(lib().ccq_synthetic_matrix(rows, cols, 0 if dist == "gaussian" else 1, seed,
+                                      _np_ptr(out) if out.size else None))
+    return out
 
 
 def _nibbles(codes: np.ndarray) -> np.ndarray:

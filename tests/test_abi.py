@@ -109,3 +109,29 @@ def test_product_does_not_reference_oracle():
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "import oracle" not in txt and "ccq_oracle" not in txt, f
                 assert "libccq_ref" not in txt, f
+
+
+def test_reference_exact_synthetic_generators(oracle):
+    """ccq_synthetic_packed / ccq_synthetic_matrix (the bench harness's
+    generators, host code in libccq_b200.so) reproduce the reference's
+    random_quantized + pack_model and random_matrix byte for byte: against
+    the C oracle restatement and, when built, the compiled reference."""
+    import numpy as np
+    from paper_2507_07145_b200.synthetic import reference_matrix, reference_packed
+    odd = {2: 65, 0: 66, 1: 57}
+    for fam in (2, 0, 1):
+        for rows, cols, gs, seed in ((37, 256, 64, 5), (14, 4096, 64, 4096 * 31 + 14336), (9, odd[fam] * 3, odd[fam], 3)):
+            a = reference_packed(rows, cols, fam, gs, seed)
+            b = oracle.random_packed(rows, cols, fam, gs, seed=seed)
+            assert np.array_equal(a.code_payload, b.code_payload)
+            assert np.array_equal(a.scale_payload, b.scale_payload)
+            for x, y in ((a.super_scales, b.super_scales), (a.cluster_scales, b.cluster_scales),
+                         (a.cluster_zero_points, b.cluster_zero_points)):
+                assert np.array_equal(np.asarray(x, np.float32).view(np.uint32), np.asarray(y, np.float32).view(np.uint32))
+            if oracle.ref_available() and gs == 64:
+                r = oracle.RefModel.random(rows, cols, fam, gs, seed).sections()
+                assert np.array_equal(a.code_payload, np.asarray(r.code_payload, np.uint8))
+    for dist in ("gaussian", "uniform"):
+        for rows, cols, seed in ((1, 4096, 4096 * 31 + 14336 + 1), (3, 7, 5)):
+            assert np.array_equal(reference_matrix(rows, cols, dist, seed).view(np.uint32),
+                                  oracle.random_matrix(rows, cols, dist, seed).view(np.uint32))
