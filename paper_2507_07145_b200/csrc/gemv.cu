@@ -166,6 +166,7 @@ struct GemvArgs {
   int streams;                 // row streams per CTA (warps = nch * streams)
   int rows_per_cta_max;
   int x_direct;                // M = 1: lanes load their group's x from global (no smem pass)
+  int x_half;                  // M = 1, 2.06, 16-bit x: stage x in shared memory as is
   // grouped experts, one token per hit expert (offsets != nullptr): the model
   // stacks E experts of rows_e rows; CTA b serves hit expert b % nhit (rows
   // split over the CTAs of that expert), reading x row offsets[e] and
@@ -585,6 +586,9 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   for (int s = 0; s < S; ++s) issue(s, s);
   TRACE(8);
   griddep_launch_dependents();
+  // the epilogue's row scale, loaded now (static data) rather than after the loop
+  const bool sup_early = nrows * MT <= int(blockDim.x);
+  const float sup_pre = sup_early && int(threadIdx.x) < nrows * MT ? L.super[r_begin + threadIdx.x / MT] : 0.f;
   griddep_wait();  // x (and y) belong to the previous kernel from here on
   TRACE(6);
 
@@ -605,6 +609,51 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
         const int p = T::perm(i);
         const float4 f = xg.v[p >> 2];
         const float xv = (p & 3) == 0 ? f.x : (p & 3) == 1 ? f.y : (p & 3) == 2 ? f.z : f.w;
+        q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xv, q4[i & 3]);
+      }
+      qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      qv[0] = 0.f;
+    }
+   } else if (FAM == kF206 && XDT != CCQ_DTYPE_F32 && a.x_half) {
+    // 2.06 with 16-bit activations: the CTA copies x into shared memory as
+    // is (16-byte pieces, XOR-swizzled by (group & 7)), each lane loads its
+    // group's 128 bytes and widens them to f32 in registers - half the shared
+    // memory reads of the f32 staging below, which 8 streams per chunk repeat.
+    uint16_t* xs16 = reinterpret_cast<uint16_t*>(xs);
+    for (int qd = threadIdx.x; qd < int(gpr) * 8; qd += blockDim.x) {
+      const int gg = qd >> 3, ch = qd & 7;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(xin) + int64_t(gg) * 64 + ch * 8));
+      *reinterpret_cast<uint4*>(xs16 + gg * 64 + ((ch ^ (gg & 7)) << 3)) = v;
+    }
+    __syncthreads();
+    if (active && a.M > 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint4 v = lds128(xs16 + g * 64 + ((k ^ (g & 7)) << 3));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if constexpr (XDT == CCQ_DTYPE_BF16) {
+            f[2 * j] = __uint_as_float(w[j] << 16);
+            f[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+          } else {
+            const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+            f[2 * j] = h.x;
+            f[2 * j + 1] = h.y;
+          }
+        }
+        xg.v[2 * k] = make_float4(f[0], f[1], f[2], f[3]);
+        xg.v[2 * k + 1] = make_float4(f[4], f[5], f[6], f[7]);
+      }
+      float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float4 f = xg.v[i >> 2];
+        const float xv = (i & 3) == 0 ? f.x : (i & 3) == 1 ? f.y : (i & 3) == 2 ? f.z : f.w;
         q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xv, q4[i & 3]);
       }
       qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
@@ -790,7 +839,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     float v = 0.f;
     for (int cc = 0; cc < nch; ++cc) v += part[(rl * nch + cc) * MT + m];
     const int64_t row = r_begin + rl;
-    v *= L.super[row];
+    v *= sup_early ? sup_pre : L.super[row];
     const int64_t yi = (tok + m) * a.y_stride + (row - row_base);
     if (a.y_dtype == CCQ_DTYPE_F32)
       static_cast<float*>(a.y)[yi] = v;
@@ -1040,6 +1089,9 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   // direct per-lane x loads win on K-heavy layers (more chunks: the shared
   // x pass grows with K), the shared pass on K <= 4096 (profiles/r02_gemv_xdirect.txt)
   static const int xd = std::getenv("CCQ_X_DIRECT") ? std::atoi(std::getenv("CCQ_X_DIRECT")) : -1;
+  static const int xh = std::getenv("CCQ_X_HALF") ? std::atoi(std::getenv("CCQ_X_HALF")) : 1;
+  a.x_half = MT == 1 && FAM == kF206 && x_dtype != CCQ_DTYPE_F32 && xh == 1 &&
+             (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && m->cols % 64 == 0;
   a.x_direct = MT == 1 && (xd == 1 || (xd < 0 && m->nch > 2)) &&
                (reinterpret_cast<uintptr_t>(x) & (x_dtype == CCQ_DTYPE_F32 ? 15u : 15u)) == 0 && m->cols % 64 == 0;
 
