@@ -249,7 +249,9 @@ int launch_grouped_gemm_tiles(const ccq_dev_model* stack, int E, int64_t rows_e,
                               int x_dtype, void* y, int y_dtype, cudaStream_t s);
 int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
                         int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
-                        int y_dtype, cudaStream_t s);
+                        int y_dtype, cudaStream_t s, int bn = 0);
+// token-tile width (64/128/160/192/256) minimising padded columns for the host routing
+int grouped_bn_for(const ccq_dev_model* stack, const int32_t* offsets_host, int E, int x_dtype);
 bool gemv_fast_supported(const ccq_dev_model* m, int64_t M);
 // Kernel (b) on the tensor pipe (gemv_mma.cu): M <= kMmaMaxTokens per launch
 // chunk, group size 64, all three families.

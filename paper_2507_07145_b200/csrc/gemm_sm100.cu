@@ -1003,6 +1003,8 @@ int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
     case kF275:
       if (xr <= 64) return run_gemm<kF275, 64>(m, x, x_dtype, M, y, y_dtype, s);
       if (xr <= 128) return run_gemm<kF275, 128>(m, x, x_dtype, M, y, y_dtype, s);
+      if (xr <= 160) return run_gemm<kF275, 160>(m, x, x_dtype, M, y, y_dtype, s);
+      if (xr <= 192) return run_gemm<kF275, 192>(m, x, x_dtype, M, y, y_dtype, s);
       return run_gemm<kF275, 256>(m, x, x_dtype, M, y, y_dtype, s);
     case kF25:  // two accumulators: at most 128 token columns per tile
       if (xr <= 64) return run_gemm<kF25, 64>(m, x, x_dtype, M, y, y_dtype, s);
@@ -1010,31 +1012,64 @@ int launch_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, v
     default:
       if (xr <= 64) return run_gemm<kF206, 64>(m, x, x_dtype, M, y, y_dtype, s);
       if (xr <= 128) return run_gemm<kF206, 128>(m, x, x_dtype, M, y, y_dtype, s);
+      if (xr <= 160) return run_gemm<kF206, 160>(m, x, x_dtype, M, y, y_dtype, s);
+      if (xr <= 192) return run_gemm<kF206, 192>(m, x, x_dtype, M, y, y_dtype, s);
       return run_gemm<kF206, 256>(m, x, x_dtype, M, y, y_dtype, s);
   }
 }
 
 // Kernel (d): all experts of a stacked model in ONE launch.  T = total tokens
 // (expert-major), max_tokens = largest per-expert token count.
+// Token-tile width for a grouped launch: with every tile MMA-bound (N >= 96),
+// the time is proportional to the padded columns sum_e ceil(n_e / BN) * BN,
+// so take the candidate that minimises them (larger on ties).  DeepSeek's
+// ~128 tokens per expert fit one 160-column tile (vs half-empty 256-column
+// ones); ERNIE's ~512 stay on 256 (profiles/r02_grouped_bn.txt).
+int grouped_bn_for(const ccq_dev_model* stack, const int32_t* offsets_host, int E, int x_dtype) {
+  const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
+  static const int cands[4] = {128, 160, 192, 256};
+  int best = 256;
+  int64_t best_cols = -1;
+  int64_t maxn = 0;
+  for (int e = 0; e < E; ++e) maxn = std::max<int64_t>(maxn, offsets_host[e + 1] - offsets_host[e]);
+  if (maxn * xs <= 64) return 64;
+  for (int c : cands) {
+    if (stack->family == kF25 && c > 128) break;  // two accumulators: <= 128 columns
+    const int tb = c / xs;
+    int64_t cols = 0;
+    for (int e = 0; e < E; ++e) cols += (int64_t(offsets_host[e + 1] - offsets_host[e]) + tb - 1) / tb * c;
+    if (best_cols < 0 || cols <= best_cols) {
+      best_cols = cols;
+      best = c;
+    }
+  }
+  return best;
+}
+
 int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const int32_t* offsets_dev,
                         int64_t T, int64_t max_tokens, const void* x, int x_dtype, void* y,
-                        int y_dtype, cudaStream_t s) {
+                        int y_dtype, cudaStream_t s, int bn) {
   if (max_tokens <= 0 || T <= 0) return CCQ_OK;
   int64_t xr = x_dtype == CCQ_DTYPE_F32 ? 2 * max_tokens : max_tokens;
   static const int force_bn = std::getenv("CCQ_GROUPED_BN") ? std::atoi(std::getenv("CCQ_GROUPED_BN")) : 0;
-  if (force_bn) xr = force_bn;
+  if (force_bn) bn = force_bn;
+  if (bn <= 0) bn = xr <= 64 ? 64 : xr <= 128 ? 128 : 256;
 #define CCQ_GROUPED(F, B) run_gemm<F, B>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens)
   switch (stack->family) {
     case kF275:
-      if (xr <= 64) return CCQ_GROUPED(kF275, 64);
-      if (xr <= 128) return CCQ_GROUPED(kF275, 128);
+      if (bn <= 64) return CCQ_GROUPED(kF275, 64);
+      if (bn <= 128) return CCQ_GROUPED(kF275, 128);
+      if (bn <= 160) return CCQ_GROUPED(kF275, 160);
+      if (bn <= 192) return CCQ_GROUPED(kF275, 192);
       return CCQ_GROUPED(kF275, 256);
     case kF25:
-      if (xr <= 64) return CCQ_GROUPED(kF25, 64);
+      if (bn <= 64) return CCQ_GROUPED(kF25, 64);
       return CCQ_GROUPED(kF25, 128);
     default:
-      if (xr <= 64) return CCQ_GROUPED(kF206, 64);
-      if (xr <= 128) return CCQ_GROUPED(kF206, 128);
+      if (bn <= 64) return CCQ_GROUPED(kF206, 64);
+      if (bn <= 128) return CCQ_GROUPED(kF206, 128);
+      if (bn <= 160) return CCQ_GROUPED(kF206, 160);
+      if (bn <= 192) return CCQ_GROUPED(kF206, 192);
       return CCQ_GROUPED(kF206, 256);
   }
 #undef CCQ_GROUPED
@@ -1045,9 +1080,10 @@ int launch_grouped_gemm(const ccq_dev_model* stack, int E, int64_t rows_e, const
 // grouped_tile_tokens(...) tokens per expert; the grid is sized for the worst
 // case (max_tiles) and CTAs past tile_prefix[E] exit at once.
 int grouped_tile_tokens(const ccq_dev_model* stack, int64_t pairs, int E, int x_dtype) {
+  // the routing is not on the host: size tiles for ~1.25x the mean tokens per expert
   const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
-  const int64_t avg = (pairs + E - 1) / std::max(E, 1) * xs;
-  int bn = avg > 96 ? 256 : (avg > 48 ? 128 : 64);
+  const int64_t typ = ((pairs + E - 1) / std::max(E, 1)) * 5 / 4 * xs;
+  int bn = typ <= 64 ? 64 : typ <= 128 ? 128 : typ <= 160 ? 160 : typ <= 192 ? 192 : 256;
   if (stack->family == kF25 && bn > 128) bn = 128;
   return bn / xs;
 }
@@ -1062,11 +1098,13 @@ int launch_grouped_gemm_tiles(const ccq_dev_model* stack, int E, int64_t rows_e,
   run_gemm<F, B>(stack, x, x_dtype, T, y, y_dtype, s, offsets_dev, rows_e, E, 0, tile_prefix_dev, max_tiles)
   switch (stack->family) {
     case kF275:
-      return bn == 64 ? CCQ_TILES(kF275, 64) : bn == 128 ? CCQ_TILES(kF275, 128) : CCQ_TILES(kF275, 256);
+      return bn == 64 ? CCQ_TILES(kF275, 64) : bn == 128 ? CCQ_TILES(kF275, 128) : bn == 160 ? CCQ_TILES(kF275, 160)
+           : bn == 192 ? CCQ_TILES(kF275, 192) : CCQ_TILES(kF275, 256);
     case kF25:
       return bn == 64 ? CCQ_TILES(kF25, 64) : CCQ_TILES(kF25, 128);
     default:
-      return bn == 64 ? CCQ_TILES(kF206, 64) : bn == 128 ? CCQ_TILES(kF206, 128) : CCQ_TILES(kF206, 256);
+      return bn == 64 ? CCQ_TILES(kF206, 64) : bn == 128 ? CCQ_TILES(kF206, 128) : bn == 160 ? CCQ_TILES(kF206, 160)
+           : bn == 192 ? CCQ_TILES(kF206, 192) : CCQ_TILES(kF206, 256);
   }
 #undef CCQ_TILES
 }

@@ -219,8 +219,14 @@ __device__ __forceinline__ float dot_206(const uint8_t* gp, const X& x, float q,
     for (int b = 0; b < 4; ++b) {
       const uint32_t qb = prmt(word, 0u, sel[b]);
       const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);
-      // IMAD.SHL (FMA pipe) measured faster than SHF here (tools/micro/dot_rate.cu)
+      // IMAD.SHL (FMA pipe) measured faster than SHF here (tools/micro/dot_rate.cu);
+      // CCQ_H2_SHF builds the ALU variant for A/B runs
+#ifdef CCQ_H2_SHF
+      uint32_t h2;
+      asm("shf.l.wrap.b32 %0, %1, %1, 6;" : "=r"(h2) : "r"(hi));  // hi < 2^23: no wrap-around bits
+#else
       const uint32_t h2 = hi << 6;
+#endif
       const float2 f01 = make_float2(fm<0x007E0000u>(hi, one), fm<0x000FC000u>(hi, one));
       const float2 f23 = make_float2(fm<0x007E0000u>(h2, one), fm<0x000FC000u>(h2, one));
       const float4 xx = x.f4(4 * wi + b);

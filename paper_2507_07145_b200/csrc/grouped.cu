@@ -123,7 +123,8 @@ extern "C" int ccq_cuda_experts_matmul(const ccq_dev_model* stack, const int32_t
     if (st != 1) return st;
   }
   if (offsets_device && gemm_supported(stack, max_tokens))
-    return launch_grouped_gemm(stack, E, re, offsets_device, T, max_tokens, x, x_dtype, y, y_dtype, s);
+    return launch_grouped_gemm(stack, E, re, offsets_device, T, max_tokens, x, x_dtype, y, y_dtype, s,
+                               grouped_bn_for(stack, offsets_host, E, x_dtype));
   // Other families: one fused decode-matmul per expert with tokens, on a
   // shallow per-expert view of the stacked device layout.
   const size_t xb = x_dtype == CCQ_DTYPE_F32 ? 4 : 2;

@@ -1,5 +1,8 @@
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-: > $OUT/disp.txt
-for f in 2.75 2.5 2.06; do for k in auto gemm; do timeout 600 python tools/time_matmul.py --family $f --shapes 4096x14336,14336x4096,4096x4096,8192x28672 --M 2,4,6,8 --kernel $k >> $OUT/disp.txt 2>&1; done; done
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gemm or prefill or experts or moe or randomized" > $OUT/pytest_bn.log 2>&1; echo "rc=$?" >> $OUT/pytest_bn.log
+: > $OUT/bn.txt
+for m in deepseek ernie; do timeout 300 python tools/gemm_knobs.py moe $m >> $OUT/bn.txt 2>&1; done
+for M in 160 192 256; do timeout 300 python tools/gemm_knobs.py dense 2.06 4096 14336 $M >> $OUT/bn.txt 2>&1; done
+for bn in 128 256; do CCQ_GROUPED_BN=$bn timeout 300 python tools/gemm_knobs.py moe deepseek >> $OUT/bn.txt 2>&1; done
