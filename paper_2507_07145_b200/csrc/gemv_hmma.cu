@@ -586,7 +586,11 @@ int launch_t(const ccq_dev_model* m, const void* x, int64_t M0, int Mn, void* y,
                        size_t(a.units_max) * kSlices * 16 * MT * 4 + 32 + 256;
   // one CTA of 32 warps per SM (64 registers each): the decode is latency
   // bound below 8 warps per scheduler (profiles/r02_hmma_*)
-  static const int warps = std::getenv("CCQ_HMMA_WARPS") ? std::atoi(std::getenv("CCQ_HMMA_WARPS")) : 32;
+  // 16 warps and two CTAs per SM (the next layer's CTA is resident and
+  // prefetches during this one) for small token counts on K <= 4096; one
+  // 32-warp CTA per SM otherwise (profiles/r02_gemv_hmma_warps.txt)
+  static const int warps_env = std::getenv("CCQ_HMMA_WARPS") ? std::atoi(std::getenv("CCQ_HMMA_WARPS")) : 0;
+  const int warps = warps_env > 0 ? warps_env : (MT <= 4 && m->nch <= 2 ? 16 : 32);
   int64_t budget = warps <= 16 ? half_sm_budget(dev) : int64_t(max_smem_optin(dev)) - 1024;
   int64_t R = (budget - int64_t(fixed) - 256) / int64_t(SB + 16);
   if (R < 4) {
