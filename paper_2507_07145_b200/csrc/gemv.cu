@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
       for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       qv[0] = 0.f;
     }
-   } else if (FAM == kF206 && XDT != CCQ_DTYPE_F32 && a.x_half) {
+   } else if (XDT != CCQ_DTYPE_F32 && a.x_half) {
     // 2.06 with 16-bit activations: the CTA copies x into shared memory as
     // is (16-byte pieces, XOR-swizzled by (group & 7)), each lane loads its
     // group's 128 bytes and widens them to f32 in registers - half the shared
@@ -636,31 +636,41 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     }
     __syncthreads();
     if (active && a.M > 0) {
+      // natural order in, the family's permuted register layout out (T::perm
+      // is compile-time: the placement is register renaming)
+      float xr[64];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint4 v = lds128(xs16 + g * 64 + ((k ^ (g & 7)) << 3));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-        float f[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if constexpr (XDT == CCQ_DTYPE_BF16) {
-            f[2 * j] = __uint_as_float(w[j] << 16);
-            f[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+            xr[8 * k + 2 * j] = __uint_as_float(w[j] << 16);
+            xr[8 * k + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
           } else {
             const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
-            f[2 * j] = h.x;
-            f[2 * j + 1] = h.y;
+            xr[8 * k + 2 * j] = h.x;
+            xr[8 * k + 2 * j + 1] = h.y;
           }
         }
-        xg.v[2 * k] = make_float4(f[0], f[1], f[2], f[3]);
-        xg.v[2 * k + 1] = make_float4(f[4], f[5], f[6], f[7]);
+      }
+#pragma unroll
+      for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const int p = T::perm(i);
+        float4& f = xg.v[p >> 2];
+        if ((p & 3) == 0) f.x = xr[i];
+        else if ((p & 3) == 1) f.y = xr[i];
+        else if ((p & 3) == 2) f.z = xr[i];
+        else f.w = xr[i];
       }
       float q4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        const float4 f = xg.v[i >> 2];
-        const float xv = (i & 3) == 0 ? f.x : (i & 3) == 1 ? f.y : (i & 3) == 2 ? f.z : f.w;
-        q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xv, q4[i & 3]);
+        if (T::exact_tail(i)) continue;
+        q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xr[i], q4[i & 3]);
       }
       qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
     } else {
@@ -1096,7 +1106,7 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   // x pass grows with K), the shared pass on K <= 4096 (profiles/r02_gemv_xdirect.txt)
   static const int xd = std::getenv("CCQ_X_DIRECT") ? std::atoi(std::getenv("CCQ_X_DIRECT")) : -1;
   static const int xh = std::getenv("CCQ_X_HALF") ? std::atoi(std::getenv("CCQ_X_HALF")) : 1;
-  a.x_half = MT == 1 && FAM == kF206 && x_dtype != CCQ_DTYPE_F32 && xh == 1 &&
+  a.x_half = MT == 1 && x_dtype != CCQ_DTYPE_F32 && xh == 1 &&
              (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && m->cols % 64 == 0;
   a.x_direct = MT == 1 && (xd == 1 || (xd < 0 && m->nch > 2)) &&
                (reinterpret_cast<uintptr_t>(x) & (x_dtype == CCQ_DTYPE_F32 ? 15u : 15u)) == 0 && m->cols % 64 == 0;

@@ -1,5 +1,6 @@
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gemv or randomized" > $OUT/pytest_hw.log 2>&1; echo "rc=$?" >> $OUT/pytest_hw.log
-timeout 600 python tools/time_matmul.py --family 2.06 --shapes 4096x14336,14336x4096,4096x4096 --M 2,4,8 > $OUT/hw_new.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gemv or baseline or randomized or experts or config" > $OUT/pytest_xh2.log 2>&1; echo "rc=$?" >> $OUT/pytest_xh2.log
+: > $OUT/xh2.txt
+for v in 0 1; do for f in 2.75 2.5; do CCQ_X_HALF=$v timeout 600 python tools/time_matmul.py --family $f --shapes 4096x14336,4096x4096 --M 1 >> $OUT/xh2.txt 2>&1; done; done
