@@ -1102,9 +1102,10 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   a.M = int(Mn);
   a.x_stride = m->cols;
   a.y_stride = m->rows;
-  // direct per-lane x loads win on K-heavy layers (more chunks: the shared
-  // x pass grows with K), the shared pass on K <= 4096 (profiles/r02_gemv_xdirect.txt)
-  static const int xd = std::getenv("CCQ_X_DIRECT") ? std::atoi(std::getenv("CCQ_X_DIRECT")) : -1;
+  // direct per-lane x loads beat the f32 shared-memory pass on K-heavy layers,
+  // but the bf16 shared-memory staging (x_half) beats both everywhere
+  // (profiles/r02_gemv_xdirect.txt): direct loads are opt-in (CCQ_X_DIRECT=1)
+  static const int xd = std::getenv("CCQ_X_DIRECT") ? std::atoi(std::getenv("CCQ_X_DIRECT")) : 0;
   static const int xh = std::getenv("CCQ_X_HALF") ? std::atoi(std::getenv("CCQ_X_HALF")) : 1;
   a.x_half = MT == 1 && x_dtype != CCQ_DTYPE_F32 && xh == 1 &&
              (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && m->cols % 64 == 0;
