@@ -166,6 +166,8 @@ struct GemvArgs {
   int streams;                 // row streams per CTA (warps = nch * streams)
   int rows_per_cta_max;
   int x_direct;                // M = 1: lanes load their group's x from global (no smem pass)
+  int tail_split;              // M = 1, 2.06: split the leftover rows' bytes across warps
+  int rows_first;              // longer row streams on the low warp ids
   int x_half;                  // M = 1, 2.06, 16-bit x: stage x in shared memory as is
   // grouped experts, one token per hit expert (offsets != nullptr): the model
   // stacks E experts of rows_e rows; CTA b serves hit expert b % nhit (rows
@@ -240,6 +242,28 @@ __device__ __forceinline__ float dot_206(const uint8_t* gp, const X& x, float q,
     }
   }
   return fmaf(64.f, a0.x + a1.x, fmaf(512.f, a0.y + a1.y, -q));
+}
+
+// dot_206 over the byte pair SL (bytes 2 SL, 2 SL + 1) of the group, without
+// the - q term: the split-row tail of gemv_stream, where the rows left over by
+// the static row split are decoded two bytes per warp.
+template <int SL, class X>
+__device__ __forceinline__ float dot_206_pair(const uint8_t* gp, const X& x, const WidenPlan& pl,
+                                              const uint32_t (&sel)[4], uint32_t one) {
+  const uint32_t word = *reinterpret_cast<const uint32_t*>(gp + 4 * (SL / 2));
+  float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int b = 2 * (SL & 1); b < 2 * (SL & 1) + 2; ++b) {
+    const uint32_t qb = prmt(word, 0u, sel[b]);
+    const uint32_t hi = uint32_t((uint64_t(qb) * pl.M + pl.C) >> 32);
+    const uint32_t h2 = hi << 6;
+    const float2 f01 = make_float2(fm<0x007E0000u>(hi, one), fm<0x000FC000u>(hi, one));
+    const float2 f23 = make_float2(fm<0x007E0000u>(h2, one), fm<0x000FC000u>(h2, one));
+    const float4 xx = x.f4(4 * (SL / 2) + b);
+    a = __ffma2_rn(f01, make_float2(xx.x, xx.y), a);
+    a = __ffma2_rn(f23, make_float2(xx.z, xx.w), a);
+  }
+  return fmaf(64.f, a.x, 512.f * a.y);
 }
 
 // 2.06 with the widening on the FP64 pipe (plan64, model.cu build_plan64):
@@ -544,6 +568,18 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   uint8_t* rings = reinterpret_cast<uint8_t*>(xbar + 2);
   uint8_t* ring = rings + size_t(warp) * S * SB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(rings + size_t(nwarps) * S * SB) + warp * S;
+  // split-row tail (M = 1, 2.06): the rows left over by the static split
+  // (nrows % streams) land, one bulk copy per chunk, in tbuf; their bytes are
+  // decoded by several warps each (tpart: per row, chunk and byte slice)
+  constexpr bool TSPLIT = MT == 1 && FAM == kF206 && !W64;
+  const bool tsplit = TSPLIT && a.tail_split;
+  const int tmax = a.streams - 1;
+  uint8_t* tbuf = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(rings + size_t(nwarps) * S * SB + size_t(nwarps) * S * 8) + 127) & ~uintptr_t(127));
+  uint64_t* tbars = reinterpret_cast<uint64_t*>(tbuf + size_t(tmax) * nch * REC);
+  float* tpart = reinterpret_cast<float*>(tbars + nch);
+  const int base_rows = nrows / a.streams;
+  const int ntail = tsplit ? nrows - base_rows * a.streams : 0;
 
   const int g0 = c * kChunk;
   const int ng = int(gpr - g0 < kChunk ? gpr - g0 : kChunk);
@@ -564,6 +600,7 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   //    L2 slices).
   if (lane == 0)
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+  if (ntail > 0 && warp < nch && lane == 0) mbar_init(&tbars[warp], 1);
   fence_mbar_init();
   __syncthreads();
 
@@ -573,8 +610,13 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   //    the grid-dependency wait (PDL): they do not depend on the previous
   //    kernel, so they overlap its tail.
   const int stream = warp / nch;
-  const int64_t w_begin = r_begin + int64_t(stream) * nrows / a.streams;
-  const int64_t w_end = r_begin + int64_t(stream + 1) * nrows / a.streams;
+  // rows_first: the streams that take one row more than the rest are the
+  // LOW warp ids (ceil split), which the warp scheduler favours - the longer
+  // streams then finish with the others instead of decoding their last row
+  // alone on an otherwise idle SM sub-partition (profiles/r02_trace_gemv_tail.txt)
+  const int64_t rb = a.rows_first ? a.streams - 1 : 0;
+  const int64_t w_begin = tsplit ? r_begin + int64_t(stream) * base_rows : r_begin + (int64_t(stream) * nrows + rb) / a.streams;
+  const int64_t w_end = tsplit ? w_begin + base_rows : r_begin + (int64_t(stream + 1) * nrows + rb) / a.streams;
   const int ntl = int((w_end - w_begin + RPW - 1) / RPW);
   const uint8_t* src = L.record(c, 0);
   const uint64_t pol = policy_evict_first();
@@ -590,6 +632,11 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
   };
 #pragma unroll
   for (int s = 0; s < S; ++s) issue(s, s);
+  if (ntail > 0 && stream == 0 && lane == 0) {  // this chunk's tail rows: one copy
+    mbar_arrive_expect_tx(&tbars[c], uint32_t(ntail) * REC);
+    bulk_g2s_evict_first(tbuf + size_t(c) * tmax * REC, src + (r_begin + int64_t(a.streams) * base_rows) * REC,
+                         uint32_t(ntail) * REC, &tbars[c], pol);
+  }
   TRACE(8);
   griddep_launch_dependents();
   // the epilogue's row scale, loaded now (static data) rather than after the loop
@@ -629,12 +676,39 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     // group's 128 bytes and widens them to f32 in registers - half the shared
     // memory reads of the f32 staging below, which 8 streams per chunk repeat.
     uint16_t* xs16 = reinterpret_cast<uint16_t*>(xs);
-    for (int qd = threadIdx.x; qd < int(gpr) * 8; qd += blockDim.x) {
-      const int gg = qd >> 3, ch = qd & 7;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(xin) + int64_t(gg) * 64 + ch * 8));
-      *reinterpret_cast<uint4*>(xs16 + gg * 64 + ((ch ^ (gg & 7)) << 3)) = v;
+    // x_half == 2: the group sums Q = sum (class + zero point) * x are formed
+    // here, once per group (8 threads x 8 activations, butterfly over the 8),
+    // instead of by every one of the nwarps / nch streams that share a chunk.
+    const bool coop_q = a.x_half == 2;
+    for (int base = int(threadIdx.x) & ~31; base < int(gpr) * 8; base += int(blockDim.x)) {
+      const int qd = base + lane, gg = qd >> 3, ch = qd & 7;
+      const bool ok = qd < int(gpr) * 8;
+      float qp = 0.f;
+      if (ok) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(xin) + int64_t(gg) * 64 + ch * 8));
+        *reinterpret_cast<uint4*>(xs16 + gg * 64 + ((ch ^ (gg & 7)) << 3)) = v;
+        if (coop_q) {
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int i = ch * 8 + j;
+            if (T::exact_tail(i)) continue;
+            const uint32_t h = (j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xFFFFu);
+            const float xv = XDT == CCQ_DTYPE_BF16 ? __uint_as_float(h << 16) : __half2float(__ushort_as_half(uint16_t(h)));
+            qp = fmaf(T::cls(i) + float(T::ZP), xv, qp);
+          }
+        }
+      }
+      if (coop_q) {
+        qp += __shfl_xor_sync(0xFFFFFFFFu, qp, 1);
+        qp += __shfl_xor_sync(0xFFFFFFFFu, qp, 2);
+        qp += __shfl_xor_sync(0xFFFFFFFFu, qp, 4);
+        if (ok && ch == 0) qs[gg] = qp;
+      }
     }
+    TRACE(9);
     __syncthreads();
+    TRACE(10);
     if (active && a.M > 0) {
       // natural order in, the family's permuted register layout out (T::perm
       // is compile-time: the placement is register renaming)
@@ -666,18 +740,23 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
         else if ((p & 3) == 2) f.z = xr[i];
         else f.w = xr[i];
       }
-      float q4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (coop_q) {
+        qv[0] = qs[g];
+      } else {
+        float q4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        if (T::exact_tail(i)) continue;
-        q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xr[i], q4[i & 3]);
+        for (int i = 0; i < 64; ++i) {
+          if (T::exact_tail(i)) continue;
+          q4[i & 3] = fmaf(T::cls(i) + float(T::ZP), xr[i], q4[i & 3]);
+        }
+        qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
       }
-      qv[0] = (q4[0] + q4[1]) + (q4[2] + q4[3]);
     } else {
 #pragma unroll
       for (int k = 0; k < T::XG / 4; ++k) xg.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       qv[0] = 0.f;
     }
+    TRACE(11);
    } else {
     // Cooperative pass straight from global memory (plain loads: they do not
     // queue behind this SM's weight bulk copies in the TMA unit): f32,
@@ -775,6 +854,8 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     for (int i = 0; i < RPW * MT; ++i) acc[i] = 0.f;
     mbar_wait(&bars[s], uint32_t((t / S) & 1));
     if (t == 0) { TRACE(2); }
+    if (t == ntl - 1) { TRACE(13); }
+    if (t == ntl - 2) { TRACE(15); }
     ++ntiles_done;
     const uint8_t* st = ring + s * SB;
     // rows of this tile (the last tile of a stream may be short): rows past
@@ -838,7 +919,44 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
       const int r = idx / MT, m = idx % MT;
       if (r0 + r < w_end) part[(int(r0 + r - r_begin) * nch + c) * MT + m] = v;
     }
+    if (t == ntl - 1) { TRACE(14); }
   }
+  }
+  if constexpr (TSPLIT) {
+    // (tail row, byte pair) items, 8 per row, dealt round-robin to the streams
+    // of this chunk
+    if (ntail > 0 && stream < ntail * 8) mbar_wait(&tbars[c], 0u);
+    for (int it = stream; it < ntail * 8; it += a.streams) {
+      const int tr = it >> 3, sl = it & 7;
+      const uint8_t* st = tbuf + (size_t(c) * tmax + tr) * REC;
+      float v = 0.f;
+      if (active) {
+        WidenPlan pl;
+        const uint4 pv = lds128(st + CGB + 16);
+        pl.C = uint64_t(pv.x) | (uint64_t(pv.y) << 32);
+        pl.M = pv.z;
+        pl.sel = pv.w;
+        const uint32_t base = pv.w & 0xFFFFu, step = pv.w >> 16;
+        const uint32_t sel[4] = {base, base + step, base + 2 * step, base + 3 * step};
+        const uint8_t* gp = st + lane * T::PB;
+        float d;
+        switch (sl) {
+          case 0: d = dot_206_pair<0>(gp, xg, pl, sel, one) - qv[0]; break;
+          case 1: d = dot_206_pair<1>(gp, xg, pl, sel, one); break;
+          case 2: d = dot_206_pair<2>(gp, xg, pl, sel, one); break;
+          case 3: d = dot_206_pair<3>(gp, xg, pl, sel, one); break;
+          case 4: d = dot_206_pair<4>(gp, xg, pl, sel, one); break;
+          case 5: d = dot_206_pair<5>(gp, xg, pl, sel, one); break;
+          case 6: d = dot_206_pair<6>(gp, xg, pl, sel, one); break;
+          default: d = dot_206_pair<7>(gp, xg, pl, sel, one); break;
+        }
+        const uint8_t nib = st[CGB + (lane >> 1)];
+        v = float((nib >> (4 * (lane & 1))) & 0xF) * d;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) tpart[(tr * nch + c) * 8 + sl] = v;
+    }
   }
   TRACE(3);
 #ifdef CCQ_GEMV_TRACE
@@ -853,7 +971,13 @@ __global__ void __launch_bounds__(512, 1) gemv_stream(GemvArgs a) {
     const int rl = e / MT, m = e % MT;
     if (m >= a.M) continue;
     float v = 0.f;
-    for (int cc = 0; cc < nch; ++cc) v += part[(rl * nch + cc) * MT + m];
+    const int tr = rl - a.streams * base_rows;
+    if (ntail > 0 && tr >= 0) {
+      for (int cc = 0; cc < nch; ++cc)
+        for (int sl = 0; sl < 8; ++sl) v += tpart[(tr * nch + cc) * 8 + sl];
+    } else {
+      for (int cc = 0; cc < nch; ++cc) v += part[(rl * nch + cc) * MT + m];
+    }
     const int64_t row = r_begin + rl;
     v *= sup_early ? sup_pre : L.super[row];
     const int64_t yi = (tok + m) * a.y_stride + (row - row_base);
@@ -1106,9 +1230,14 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   // but the bf16 shared-memory staging (x_half) beats both everywhere
   // (profiles/r02_gemv_xdirect.txt): direct loads are opt-in (CCQ_X_DIRECT=1)
   static const int xd = std::getenv("CCQ_X_DIRECT") ? std::atoi(std::getenv("CCQ_X_DIRECT")) : 0;
-  static const int xh = std::getenv("CCQ_X_HALF") ? std::atoi(std::getenv("CCQ_X_HALF")) : 1;
-  a.x_half = MT == 1 && x_dtype != CCQ_DTYPE_F32 && xh == 1 &&
-             (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && m->cols % 64 == 0;
+  static const int xh = std::getenv("CCQ_X_HALF") ? std::atoi(std::getenv("CCQ_X_HALF")) : 2;
+  a.x_half = MT == 1 && x_dtype != CCQ_DTYPE_F32 && xh >= 1 &&
+             (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && m->cols % 64 == 0 ? xh : 0;
+  static const int ts = std::getenv("CCQ_GEMV_TAIL") ? std::atoi(std::getenv("CCQ_GEMV_TAIL")) : 1;
+  const bool tsplit_ok = MT == 1 && FAM == kF206 && !W64 && ts == 1;
+  a.tail_split = tsplit_ok;
+  static const int rf = std::getenv("CCQ_GEMV_ROWS_FIRST") ? std::atoi(std::getenv("CCQ_GEMV_ROWS_FIRST")) : 1;
+  a.rows_first = rf;
   a.x_direct = MT == 1 && (xd == 1 || (xd < 0 && m->nch > 2)) &&
                (reinterpret_cast<uintptr_t>(x) & (x_dtype == CCQ_DTYPE_F32 ? 15u : 15u)) == 0 && m->cols % 64 == 0;
 
@@ -1137,9 +1266,14 @@ int launch_stream_dt(const ccq_dev_model* m, const void* x, int x_dtype, int64_t
   // As many row streams as the register file (16 warps) and shared memory allow.
   size_t smem = 0;
   int warps = 0;
-  for (a.streams = std::max(1, 16 / m->nch); a.streams >= 1; --a.streams) {
+  static const int max_streams = std::getenv("CCQ_GEMV_STREAMS") ? std::atoi(std::getenv("CCQ_GEMV_STREAMS")) : 0;
+  const int s0 = std::max(1, 16 / m->nch);
+  for (a.streams = max_streams > 0 ? std::min(max_streams, s0) : s0; a.streams >= 1; --a.streams) {
     warps = m->nch * a.streams;
     smem = pbytes + xbytes + 64 + 16 + xraw + size_t(warps) * S * SB + size_t(warps) * S * 8 + 128;
+    if (tsplit_ok)  // split-row tail: records, barriers, partials (+ alignment)
+      smem += 128 + size_t(a.streams - 1) * m->nch * (size_t(SB) / RPW) + size_t(m->nch) * 8 +
+              size_t(a.streams - 1) * m->nch * 32;
     if (smem <= size_t(max_smem)) break;
   }
   if (a.streams < 1) return fail(CCQ_ERR_CONFIG, "shared memory budget exceeded in the streaming GEMV");

@@ -809,7 +809,8 @@ def test_matmul_rejects_bad_output_buffers(oracle, ccq, cuda):
 def test_fp64_widening_variant_subprocess(cuda):
     """The opt-in FP64-pipe widening (CCQ_W64=1: plans built and verified at
     upload, gemv_stream's dot_206_w64) gives the same M = 1 products as the
-    default IMAD.WIDE plan path (bit for bit: same fields, same float ops)."""
+    default IMAD.WIDE plan path (bit for bit: same fields, same float ops;
+    the split-row tail, which the W64 build does not take, is off in both)."""
     import subprocess
     import sys
     from conftest import ROOT
@@ -826,7 +827,7 @@ def test_fp64_widening_variant_subprocess(cuda):
         import os
         import tempfile
         path = os.path.join(tempfile.mkdtemp(), name)
-        r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, CCQ_W64=w64),
+        r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, CCQ_W64=w64, CCQ_GEMV_TAIL="0"),
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))

@@ -40,7 +40,7 @@ loop = rel[:, 9] - rel[:, 8]
 print(f"loop time per warp: p50 {np.median(loop):.2f} max {loop.max():.2f} us; per tile p50 {np.median(loop / np.maximum(t[:, 5], 1)):.3f} us")
 
 # per-CTA view: slowest warp loop end per CTA vs SM id (die locality / imbalance)
-wpc = 16
+wpc = int(os.environ.get("WPC", "16"))
 nct = t.shape[0] // wpc
 cta_end = rel[: nct * wpc, 9].reshape(nct, wpc).max(1)
 cta_first = rel[: nct * wpc, 8].reshape(nct, wpc).min(1)
@@ -51,3 +51,21 @@ print(" ".join(f"{int(smid[i])}:{cta_end[i]:.1f}" for i in order))
 lo = smid < 74
 print(f"SM<74 mean end {cta_end[lo].mean():.2f} max {cta_end[lo].max():.2f}; SM>=74 mean {cta_end[~lo].mean():.2f} max {cta_end[~lo].max():.2f}")
 print(f"first data by SM half: {cta_first[lo].mean():.2f} / {cta_first[~lo].mean():.2f}")
+# row-balance tail: CTAs whose slowest stream has one more tile (97- vs 96-row CTAs)
+cta_tiles = t[: nct * wpc, 5].reshape(nct, wpc).max(1)
+for k in np.unique(cta_tiles):
+    sel = cta_tiles == k
+    print(f"CTAs with max {int(k)} tiles/warp: {int(sel.sum())}, loop-end mean {cta_end[sel].mean():.2f} max {cta_end[sel].max():.2f}")
+wt = t[:, 5]
+for k in np.unique(wt):
+    sel = wt == k
+    print(f"warps with {int(k)} tiles: {int(sel.sum())}, loop end p50 {np.median(rel[sel, 9]):.2f}, loop time p50 {np.median(loop[sel]):.2f}")
+# last / penultimate tile timing (slots 15 = penultimate tile data ready, 13 = last tile data ready, 14 = last tile done)
+pen = (t[:, 15] - base) / 1000.0
+lst = (t[:, 13] - base) / 1000.0
+lend = (t[:, 14] - base) / 1000.0
+for k in np.unique(wt):
+    sel = wt == k
+    print(f"{int(k)}-tile warps: penult start p50 {np.median(pen[sel]):.2f}, last start p50 {np.median(lst[sel]):.2f}, "
+          f"last end p50 {np.median(lend[sel]):.2f}; last tile dur p50 {np.median(lend[sel] - lst[sel]):.3f}, "
+          f"penult tile dur p50 {np.median(lst[sel] - pen[sel]):.3f}")
