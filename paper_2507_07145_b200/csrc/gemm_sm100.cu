@@ -326,12 +326,6 @@ struct GemmSmem {
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
-__device__ __forceinline__ void store_y(const GemmArgs& a, int64_t idx, float out) {
-  if (a.y_dtype == CCQ_DTYPE_F32)
-    static_cast<float*>(a.y)[idx] = out;
-  else
-    static_cast<__nv_bfloat16*>(a.y)[idx] = __float2bfloat16_rn(out);
-}
 
 
 // f16 bit pattern of a small non-negative integer (exact below 2048).
@@ -801,33 +795,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(fmaf(64.f, __uint_as_float(vh[i]), __uint_as_float(v[i])));
       }
       tmem_ld_wait();
-      if (row < row_end && a.partial) {
-        // split-K: raw sums (hi + lo parts for f32 inputs), scaled by the reduce kernel
-        float* pz = a.partial + size_t(blockIdx.z) * size_t(a.M) * size_t(a.rows);
-        const int per = 32 / a.xs;
-#pragma unroll 1
-        for (int i = 0; i < per; ++i) {
-          const int64_t n = n0 + (cc / a.xs) + i;
-          if (n < tok_end) {
-            const float v0 = a.xs == 1 ? __uint_as_float(v[i]) : __uint_as_float(v[2 * i]) + __uint_as_float(v[2 * i + 1]);
-            pz[n * a.rows + row] = v0;
-          }
-        }
-      } else if (row < row_end) {
-        if (a.xs == 1) {
+      // Lanes are consecutive rows: one 128 B (f32) / 64 B (bf16) store per
+      // token and warp.  The token scales are loaded once per slice (one per
+      // lane) and broadcast by shuffles - a per-element load behind a store
+      // to y (which may alias it) serialised one L1 round trip per element
+      // (profiles/r02_gemm_epilogue.txt).  f32 inputs: hi + lo columns first.
+      if (a.xs == 2) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t n = n0 + cc + i;
-            if (n < tok_end) store_y(a, n * y_ld + (row - y_col0), __uint_as_float(v[i]) * sup * a.inv_scale[n]);
-          }
-        } else {
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[2 * i]) + __uint_as_float(v[2 * i + 1]));
+      }
+      const int per = 32 / a.xs;          // tokens in this slice
+      const int64_t nb = n0 + cc / a.xs;  // its first token
+      const bool rok = row < row_end;
+      float* const pz = a.partial ? a.partial + size_t(blockIdx.z) * size_t(a.M) * size_t(a.rows) + row : nullptr;
+      // split-K: raw sums to the partial buffer, scaled by the reduce kernel
+      const float isc = a.partial ? 1.f : (lane < per && nb + lane < tok_end ? __ldg(a.inv_scale + nb + lane) : 0.f);
+      const float rs = a.partial ? 1.f : sup;
+      const int64_t ycol = row - y_col0;
+      const bool f32 = a.partial || a.y_dtype == CCQ_DTYPE_F32;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int64_t n = n0 + (cc >> 1) + i;
-            if (n < tok_end)
-              store_y(a, n * y_ld + (row - y_col0),
-                      (__uint_as_float(v[2 * i]) + __uint_as_float(v[2 * i + 1])) * sup * a.inv_scale[n]);
-          }
+      for (int i = 0; i < 32; ++i) {
+        const float si = __shfl_sync(0xffffffffu, isc, i) * rs;
+        if (i < per && rok && nb + i < tok_end) {
+          const float o = __uint_as_float(v[i]) * si;
+          if (pz) pz[(nb + i) * a.rows] = o;
+          else if (f32) static_cast<float*>(a.y)[(nb + i) * y_ld + ycol] = o;
+          else static_cast<__nv_bfloat16*>(a.y)[(nb + i) * y_ld + ycol] = __float2bfloat16_rn(o);
         }
       }
     }
