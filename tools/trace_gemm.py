@@ -19,7 +19,7 @@ from paper_2507_07145_b200.synthetic import random_packed  # noqa: E402
 Ms = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "16").split(",")]
 exps = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "0").split(",")]
 fam = os.environ.get("FAM", "2.06")
-din, dout = 4096, 14336
+din, dout = int(os.environ.get("DIN", "4096")), int(os.environ.get("DOUT", "14336"))
 m = P.DeviceModel.upload(random_packed(dout, din, P.FAMILIES[fam], 64, 3))
 for M in Ms:
     x = torch.randn(M, din, device="cuda").to(torch.bfloat16)

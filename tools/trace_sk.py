@@ -1,7 +1,7 @@
-"""Stream-K GEMM timeline per CTA (trace build): start, first stage, segment
-ends (MMA commits), epilogue ends, CTA end.  Also checks the result against
-the non-stream-K path (CCQ_GEMM_SK=0 in a subprocess is not needed: the
-matmul of the same inputs via kernel='gemm' is compared with gemv output).
+"""Stream-K GEMM timeline per CTA (trace build of the stream-K experiment:
+apply tools/experiments/gemm_streamk.patch first - the adopted kernel has no
+ccq_gemm_sktrace_dump): start, first stage, segment ends (MMA commits),
+epilogue phases, CTA end (profiles/r02_gemm_streamk.txt).
 
   python tools/trace_sk.py FAM D_IN D_OUT M
 """
