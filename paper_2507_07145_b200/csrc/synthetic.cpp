@@ -90,7 +90,7 @@ extern "C" int ccq_synthetic_packed(int64_t rows, int64_t cols, int32_t family, 
 // random_matrix (tensor.cpp:37-69): dist 0 = Gaussian (Box-Muller on
 // unit_double pairs, u1 redrawn while <= 0, cos then sin), 1 = uniform [-1, 1).
 extern "C" int ccq_synthetic_matrix(int64_t rows, int64_t cols, int32_t dist, uint64_t seed, float* out) {
-  if (rows < 0 || cols < 0 || (rows * cols && !out)) return ccqb::fail(CCQ_ERR_INVALID, "bad matrix arguments");
+  if (rows < 0 || cols < 0 || (rows * cols != 0 && !out)) return ccqb::fail(CCQ_ERR_INVALID, "bad matrix arguments");
   std::mt19937_64 rng(seed);
   const size_t n = size_t(rows) * size_t(cols);
   if (dist == 1) {
