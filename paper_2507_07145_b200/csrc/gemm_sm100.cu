@@ -82,15 +82,20 @@ constexpr int kBM = 128;        // weight rows per tile (UMMA M)
 constexpr int kBK = 64;         // K per block = one group
 constexpr int kStagesC = 5;     // packed-code ring (8 groups per stage)
 constexpr int kCodeBox = 128;   // bytes of codes per row per code stage (8 groups x 16 B)
-constexpr int kPar = 3;         // decode warp groups (K blocks kb % kPar)
-constexpr int kDecWarps = 4 * kPar;  // x 4 TMEM lane quadrants
-constexpr int kThreads = 32 * kDecWarps + 128;
-// Warp roles: decode warps first, control warps LAST - the SM warp scheduler
-// prefers the highest warp id among eligible warps, and the single MMA
-// issuing thread must not be starved by the decode warps on its sub-partition.
-constexpr int kWarpCodes = kDecWarps;      // TMA producer: packed codes
-constexpr int kWarpB = kDecWarps + 1;      // TMA producer: activation tiles
-constexpr int kWarpMma = kDecWarps + 2;    // TMEM alloc + MMA issue
+// PAR decode warp groups (K-block stages st % PAR), 4 warps each (one per
+// TMEM lane quadrant); then 4 control warps.  Warp roles: decode warps first,
+// control warps LAST - the SM warp scheduler prefers the highest warp id among
+// eligible warps, and the single MMA issuing thread must not be starved by the
+// decode warps on its sub-partition.
+//   warp 4 PAR      TMA producer: packed codes
+//   warp 4 PAR + 1  TMA producer: activation tiles
+//   warp 4 PAR + 2  TMEM alloc + MMA issue
+template <int PAR>
+struct Roles {
+  static constexpr int kDecWarps = 4 * PAR;
+  static constexpr int kThreads = 32 * kDecWarps + 128;
+  static constexpr int kWarpCodes = kDecWarps, kWarpB = kDecWarps + 1, kWarpMma = kDecWarps + 2;
+};
 constexpr int kACols = kBK / 2; // TMEM columns per A stage (two f16 per column)
 
 // ---------------------------------------------------------------------------
@@ -299,31 +304,42 @@ struct GF<kF25> {
 // groups per stage.  (Measured: a deeper 2*kPar-stage ring with G = 2 did not
 // help small M and slowed the grouped MoE GEMM by 15 %.)
 // TMEM: SPLIT*BN + SA*G*SPLIT*32 <= 512.
-template <int FAM, int BN>
+//
+// More decode warp groups (PAR > 3): the decode warps are latency-bound at
+// three per SM sub-partition (profiles/r02_gemm_bound.txt: decoding one group
+// per thread takes ~870 cycles while the ALU pipe is half idle), so wider
+// variants run PAR groups over a ring of SA = PAR one-group stages.  A group
+// handles every PAR-th stage and waits on its slot's `empty` barrier by
+// phase parity, which is only sound while PAR <= SA (otherwise the barrier
+// can be two phases behind and the parity test passes early).  The code ring
+// shrinks to what shared memory leaves (>= 3 blocks = 24 K blocks ahead).
+template <int FAM, int BN, int PAR>
 constexpr int groups_per_stage() {
+  if constexpr (PAR > 3) return BN <= 64 ? 2 : 1;
   return GF<FAM>::SPLIT == 2 ? (BN <= 64 ? 2 : 1) : (BN <= 64 ? 4 : (BN <= 128 ? 2 : 1));
 }
-template <int FAM, int BN>
-constexpr int stages_a() { return BN <= 64 ? 3 : 4; }
+template <int FAM, int BN, int PAR>
+constexpr int stages_a() { return PAR > 3 ? PAR : (BN <= 64 ? 3 : 4); }
 
-template <int FAM, int BN>
+template <int FAM, int BN, int PAR = 3>
 struct GemmSmem {
-  static constexpr int SA = stages_a<FAM, BN>();
+  static constexpr int SA = stages_a<FAM, BN, PAR>();
   static constexpr int SB = SA;
-  static constexpr int G = groups_per_stage<FAM, BN>();
-  static constexpr int SC = GF<FAM>::STAGES_C;
+  static constexpr int G = groups_per_stage<FAM, BN, PAR>();
   static constexpr int B_BLOCK = BN * kBK * 2;               // BN x 128 B per group
   static constexpr int B_BYTES = G * B_BLOCK;
   static constexpr int C_BYTES = kBM * GF<FAM>::BOXB;        // 128 rows x 8 groups of codes
   static constexpr int N_BYTES = GF<FAM>::NIB ? kBM * 16 : 0;  // side-band nibbles (2.06)
+  static constexpr int SC_FIT = (232448 - 1536 - SB * B_BYTES) / (C_BYTES + N_BYTES);
+  static constexpr int SC = SC_FIT < GF<FAM>::STAGES_C ? SC_FIT : GF<FAM>::STAGES_C;
+  static constexpr bool OK = SC >= 3 && PAR <= SA &&
+                             GF<FAM>::SPLIT * BN + SA * G * GF<FAM>::SPLIT * kACols <= 512;
   static constexpr int OFF_B = 0;                            // 1024-aligned
   static constexpr int OFF_C = OFF_B + SB * B_BYTES;
   static constexpr int OFF_N = OFF_C + SC * C_BYTES;
   static constexpr int OFF_BAR = OFF_N + SC * N_BYTES;
   static constexpr int TOTAL = OFF_BAR + 512 + 1024;  // + alignment slack
   static constexpr int TMEM_NEED = GF<FAM>::SPLIT * BN + SA * G * GF<FAM>::SPLIT * kACols;
-  static_assert(TMEM_NEED <= 512, "TMEM budget");
-  static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
 
@@ -430,11 +446,14 @@ __device__ __forceinline__ void decode_gemm_25(const uint8_t* gb, uint32_t (&hl)
   }
 }
 
-template <int FAM, int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int FAM, int BN, int PAR>
+__global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
     gemm_ccq(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
              const __grid_constant__ CUtensorMap tm_x, GemmArgs a) {
-  using SM = GemmSmem<FAM, BN>;
+  using SM = GemmSmem<FAM, BN, PAR>;
+  static_assert(SM::OK && SM::TMEM_NEED <= 512 && SM::TOTAL <= 232448, "ring does not fit");
+  constexpr int kPar = PAR, kDecWarps = Roles<PAR>::kDecWarps;
+  constexpr int kWarpCodes = Roles<PAR>::kWarpCodes, kWarpB = Roles<PAR>::kWarpB, kWarpMma = Roles<PAR>::kWarpMma;
   constexpr int SA = SM::SA, SB = SM::SB, G = SM::G;
   constexpr int SPLIT = GF<FAM>::SPLIT;
   constexpr int kStagesC = SM::SC;
@@ -573,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (GF<FAM>::NIB) tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
       }
 #ifdef CCQ_GEMM_TRACE
-      if (blockIdx.x == 0 && blockIdx.y < 320) g_gtrace2[(blockIdx.y * kDecWarps) * 4 + 3] = pw;
+      if (blockIdx.x == 0 && blockIdx.y < 3840 / kDecWarps) g_gtrace2[(blockIdx.y * kDecWarps) * 4 + 3] = pw;
 #endif
     }
   } else if (warp == kWarpMma) {
@@ -624,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit_warp(tmem_full);
 #ifdef CCQ_GEMM_TRACE
-      if (lane == 0 && blockIdx.x == 0 && blockIdx.y < 320) {
+      if (lane == 0 && blockIdx.x == 0 && blockIdx.y < 3840 / kDecWarps) {
         const int slot = (blockIdx.y * kDecWarps) * 8;
         g_gtrace[slot + 5] = wa; g_gtrace[slot + 6] = wb; g_gtrace[slot + 7] = gclk() - t0m;
       }
@@ -769,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     release_until((nkb + 7) >> 3);
 #ifdef CCQ_GEMM_TRACE
-    if (lane == 0 && blockIdx.x == 0 && blockIdx.y < 320) {
+    if (lane == 0 && blockIdx.x == 0 && blockIdx.y < 3840 / kDecWarps) {
       const int slot = (blockIdx.y * kDecWarps + warp) * 8;
       g_gtrace[slot + 0] = t_code; g_gtrace[slot + 1] = t_dec; g_gtrace[slot + 2] = t_empty;
       g_gtrace[slot + 3] = t_st; g_gtrace[slot + 4] = gclk() - t0;
@@ -849,11 +868,11 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ p
   }
 }
 
-template <int FAM, int BN>
-int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
-            cudaStream_t s, const int32_t* offsets_dev = nullptr, int64_t rows_e = 0, int E = 0,
-            int64_t max_tokens = 0, const int32_t* tile_prefix = nullptr, int64_t max_tiles = 0) {
-  using SM = GemmSmem<FAM, BN>;
+template <int FAM, int BN, int PAR>
+int run_gemm_p(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+               cudaStream_t s, const int32_t* offsets_dev, int64_t rows_e, int E,
+               int64_t max_tokens, const int32_t* tile_prefix, int64_t max_tiles) {
+  using SM = GemmSmem<FAM, BN, PAR>;
   const int64_t K = m->cols;
   const bool grouped = offsets_dev != nullptr;
   const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
@@ -906,7 +925,7 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
              offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr,
              tile_prefix, E, 0, 0, 0};
-  auto kern = gemm_ccq<FAM, BN>;
+  auto kern = gemm_ccq<FAM, BN, PAR>;
   if (int st2 = ensure_smem(reinterpret_cast<const void*>(kern), SM::TOTAL)) {
     cudaFreeAsync(x16, s);
     return st2;
@@ -959,7 +978,7 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
     }
   }
   if (grid.x && grid.y) {
-    cudaError_t le = launch_pdl(kern, grid, dim3(kThreads), SM::TOTAL, s, tm_codes, tm_nib, tm_x, a);
+    cudaError_t le = launch_pdl(kern, grid, dim3(Roles<PAR>::kThreads), SM::TOTAL, s, tm_codes, tm_nib, tm_x, a);
     count_launch();
     if (le == cudaSuccess && part) {
       const int64_t total = M * m->rows;
@@ -978,6 +997,41 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
   if (part) cudaFreeAsync(part, s);
   cudaFreeAsync(x16, s);
   return e == cudaSuccess ? CCQ_OK : cuda_fail(e, "gemm launch");
+}
+
+// Decode warp groups per CTA (PAR, see groups_per_stage): CCQ_GEMM_PAR
+// overrides the default; variants are compiled where their ring fits and the
+// register budget (65536 / threads) holds the decoder without spills.
+template <int FAM, int BN, int PAR>
+constexpr bool par_built() {
+  if constexpr (PAR == 3) return true;
+  if constexpr (!GemmSmem<FAM, BN, PAR>::OK || BN < 128) return false;
+  if constexpr (FAM == kF206) return PAR == 4 || PAR == 5 || PAR == 6;
+  if constexpr (FAM == kF275) return BN >= 160 && (PAR == 4 || PAR == 6);
+  return false;
+}
+inline int gemm_par_default(int fam, int bn) {
+  (void)fam;
+  (void)bn;
+  return 3;
+}
+template <int FAM, int BN>
+int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
+             cudaStream_t s, const int32_t* offsets_dev = nullptr, int64_t rows_e = 0, int E = 0,
+             int64_t max_tokens = 0, const int32_t* tile_prefix = nullptr, int64_t max_tiles = 0) {
+  static const int force_par = std::getenv("CCQ_GEMM_PAR") ? std::atoi(std::getenv("CCQ_GEMM_PAR")) : 0;
+  const int par = force_par > 0 ? force_par : gemm_par_default(FAM, BN);
+#define CCQ_PAR(P)                                                                                       \
+  if constexpr (par_built<FAM, BN, P>())                                                                 \
+    if (par == P)                                                                                        \
+      return run_gemm_p<FAM, BN, P>(m, x, x_dtype, M, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens, \
+                                    tile_prefix, max_tiles);
+  CCQ_PAR(4)
+  CCQ_PAR(5)
+  CCQ_PAR(6)
+#undef CCQ_PAR
+  return run_gemm_p<FAM, BN, 3>(m, x, x_dtype, M, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens, tile_prefix,
+                                max_tiles);
 }
 
 }  // namespace
