@@ -1010,9 +1010,11 @@ constexpr bool par_built() {
   if constexpr (FAM == kF275) return BN >= 160 && (PAR == 4 || PAR == 6);
   return false;
 }
+// Measured per family and tile width (profiles/r02_gemm_par.txt: dense
+// 4096 -> 14336 at M = 128..256, configs[4] prefill, grouped prefill).
 inline int gemm_par_default(int fam, int bn) {
-  (void)fam;
-  (void)bn;
+  if (fam == kF206) return bn == 128 ? 4 : bn == 160 ? 5 : bn == 192 ? 6 : bn == 256 ? 4 : 3;
+  if (fam == kF275) return bn == 160 || bn == 192 ? 6 : bn == 256 ? 4 : 3;
   return 3;
 }
 template <int FAM, int BN>
