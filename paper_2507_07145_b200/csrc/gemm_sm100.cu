@@ -90,9 +90,9 @@ constexpr int kCodeBox = 128;   // bytes of codes per row per code stage (8 grou
 //   warp 4 PAR      TMA producer: packed codes
 //   warp 4 PAR + 1  TMA producer: activation tiles
 //   warp 4 PAR + 2  TMEM alloc + MMA issue
-template <int PAR>
+template <int PAR, int RT = 1>
 struct Roles {
-  static constexpr int kDecWarps = 4 * PAR;
+  static constexpr int kDecWarps = 4 * RT * PAR;
   static constexpr int kThreads = 32 * kDecWarps + 128;
   static constexpr int kWarpCodes = kDecWarps, kWarpB = kDecWarps + 1, kWarpMma = kDecWarps + 2;
 };
@@ -313,33 +313,46 @@ struct GF<kF25> {
 // phase parity, which is only sound while PAR <= SA (otherwise the barrier
 // can be two phases behind and the parity test passes early).  The code ring
 // shrinks to what shared memory leaves (>= 3 blocks = 24 K blocks ahead).
-template <int FAM, int BN, int PAR>
+//
+// Two row tiles per CTA (RT = 2, 256 weight rows): both tiles' MMAs read the
+// same activation stage, halving the L2 -> SM traffic of the activation
+// operand per FLOP (1 B per 128 FLOP at RT = 1, which at the tensor rate is
+// ~10-12 TB/s of crossbar reads: profiles/r02_gemm_l2.txt).  Decode groups
+// are then 8 warps (2 tiles x 4 lane quadrants); TMEM holds 2 BN accumulator
+// columns + SA stages of 2 x 32 A columns, so RT = 2 exists for BN <= 160.
+template <int FAM, int BN, int PAR, int RT = 1>
 constexpr int groups_per_stage() {
+  if constexpr (RT > 1) return 1;
   if constexpr (PAR > 3) return BN <= 64 ? 2 : 1;
   return GF<FAM>::SPLIT == 2 ? (BN <= 64 ? 2 : 1) : (BN <= 64 ? 4 : (BN <= 128 ? 2 : 1));
 }
-template <int FAM, int BN, int PAR>
-constexpr int stages_a() { return PAR > 3 ? PAR : (BN <= 64 ? 3 : 4); }
+template <int FAM, int BN, int PAR, int RT = 1>
+constexpr int stages_a() {
+  if constexpr (RT > 1) return (512 - RT * BN) / (RT * 32) < 4 ? (512 - RT * BN) / (RT * 32) : 4;
+  return PAR > 3 ? PAR : (BN <= 64 ? 3 : 4);
+}
 
-template <int FAM, int BN, int PAR = 3>
+template <int FAM, int BN, int PAR = 3, int RT = 1>
 struct GemmSmem {
-  static constexpr int SA = stages_a<FAM, BN, PAR>();
+  static constexpr int SA = stages_a<FAM, BN, PAR, RT>();
   static constexpr int SB = SA;
-  static constexpr int G = groups_per_stage<FAM, BN, PAR>();
+  static constexpr int G = groups_per_stage<FAM, BN, PAR, RT>();
   static constexpr int B_BLOCK = BN * kBK * 2;               // BN x 128 B per group
   static constexpr int B_BYTES = G * B_BLOCK;
-  static constexpr int C_BYTES = kBM * GF<FAM>::BOXB;        // 128 rows x 8 groups of codes
-  static constexpr int N_BYTES = GF<FAM>::NIB ? kBM * 16 : 0;  // side-band nibbles (2.06)
+  static constexpr int C_BOX = kBM * GF<FAM>::BOXB;          // 128 rows x 8 groups of codes
+  static constexpr int N_BOX = GF<FAM>::NIB ? kBM * 16 : 0;  // side-band nibbles (2.06)
+  static constexpr int C_BYTES = RT * C_BOX;                 // one code stage: RT boxes
+  static constexpr int N_BYTES = RT * N_BOX;
   static constexpr int SC_FIT = (232448 - 1536 - SB * B_BYTES) / (C_BYTES + N_BYTES);
   static constexpr int SC = SC_FIT < GF<FAM>::STAGES_C ? SC_FIT : GF<FAM>::STAGES_C;
-  static constexpr bool OK = SC >= 3 && PAR <= SA &&
-                             GF<FAM>::SPLIT * BN + SA * G * GF<FAM>::SPLIT * kACols <= 512;
+  static constexpr bool OK = SC >= 3 && PAR <= SA && SA >= 2 && (RT == 1 || GF<FAM>::SPLIT == 1) &&
+                             RT * GF<FAM>::SPLIT * BN + SA * G * RT * GF<FAM>::SPLIT * kACols <= 512;
   static constexpr int OFF_B = 0;                            // 1024-aligned
   static constexpr int OFF_C = OFF_B + SB * B_BYTES;
   static constexpr int OFF_N = OFF_C + SC * C_BYTES;
   static constexpr int OFF_BAR = OFF_N + SC * N_BYTES;
   static constexpr int TOTAL = OFF_BAR + 512 + 1024;  // + alignment slack
-  static constexpr int TMEM_NEED = GF<FAM>::SPLIT * BN + SA * G * GF<FAM>::SPLIT * kACols;
+  static constexpr int TMEM_NEED = RT * GF<FAM>::SPLIT * BN + SA * G * RT * GF<FAM>::SPLIT * kACols;
 };
 
 
@@ -446,14 +459,15 @@ __device__ __forceinline__ void decode_gemm_25(const uint8_t* gb, uint32_t (&hl)
   }
 }
 
-template <int FAM, int BN, int PAR>
-__global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
+template <int FAM, int BN, int PAR, int RT>
+__global__ void __launch_bounds__(Roles<PAR, RT>::kThreads, 1)
     gemm_ccq(const __grid_constant__ CUtensorMap tm_codes, const __grid_constant__ CUtensorMap tm_nib,
              const __grid_constant__ CUtensorMap tm_x, GemmArgs a) {
-  using SM = GemmSmem<FAM, BN, PAR>;
+  using SM = GemmSmem<FAM, BN, PAR, RT>;
+  using RL = Roles<PAR, RT>;
   static_assert(SM::OK && SM::TMEM_NEED <= 512 && SM::TOTAL <= 232448, "ring does not fit");
-  constexpr int kPar = PAR, kDecWarps = Roles<PAR>::kDecWarps;
-  constexpr int kWarpCodes = Roles<PAR>::kWarpCodes, kWarpB = Roles<PAR>::kWarpB, kWarpMma = Roles<PAR>::kWarpMma;
+  constexpr int kPar = PAR, kDecWarps = RL::kDecWarps, kRows = kBM * RT;
+  constexpr int kWarpCodes = RL::kWarpCodes, kWarpB = RL::kWarpB, kWarpMma = RL::kWarpMma;
   constexpr int SA = SM::SA, SB = SM::SB, G = SM::G;
   constexpr int SPLIT = GF<FAM>::SPLIT;
   constexpr int kStagesC = SM::SC;
@@ -505,8 +519,8 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
       t = blockIdx.y % a.tpe;
       jt = int(blockIdx.x);
     }
-    r0 = e * a.rows_e + int64_t(t) * kBM;
-    row_end = (e + 1) * a.rows_e < r0 + kBM ? (e + 1) * a.rows_e : r0 + kBM;
+    r0 = e * a.rows_e + int64_t(t) * kRows;
+    row_end = (e + 1) * a.rows_e < r0 + kRows ? (e + 1) * a.rows_e : r0 + kRows;
     n0 = a.offsets[e] + jt * tb;
     tok_end = a.offsets[e + 1];
     if (n0 >= tok_end) return;  // expert without (more) tokens: no work, no bytes
@@ -521,8 +535,8 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
       br = first + (pid % per_group) % gsz;
       bt = (pid % per_group) / gsz;
     }
-    r0 = int64_t(br) * kBM;
-    row_end = a.rows < r0 + kBM ? a.rows : r0 + kBM;
+    r0 = int64_t(br) * kRows;
+    row_end = a.rows < r0 + kRows ? a.rows : r0 + kRows;
     n0 = bt * tb;
     tok_end = a.M;
     y_ld = a.rows;
@@ -533,7 +547,7 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&full[s], 5);  // 4 decode warps (one elected lane each) + 1 TMA arrival
+      mbar_init(&full[s], 4 * RT + 1);  // 4 RT decode warps (one elected lane each) + 1 TMA arrival
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kStagesC; ++s) {
@@ -552,8 +566,8 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_d = *tmem_slot;        // accumulator(s): columns [0, SPLIT * BN)
-  const uint32_t tmem_a = tmem_d + SPLIT * BN;  // A stages: SA x G x SPLIT x kACols columns
+  const uint32_t tmem_d = *tmem_slot;             // accumulator(s): columns [0, RT * SPLIT * BN)
+  const uint32_t tmem_a = tmem_d + RT * SPLIT * BN;  // A stages: SA x G x RT x SPLIT x kACols columns
   const int nst = (nkb + G - 1) / G;          // pipeline stages (G groups each)
 
   if (warp == kWarpB) {
@@ -585,11 +599,17 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
 #ifdef CCQ_GEMM_TRACE
         pw += gclk() - tp;
 #endif
-        mbar_arrive_expect_tx(&code_full[cs], SM::C_BYTES + SM::N_BYTES);
+        // RT boxes of 128 rows; a second box with no row of this tile is not loaded
+        const int nbox = RT > 1 && r0 + kBM >= row_end ? 1 : RT;
+        mbar_arrive_expect_tx(&code_full[cs], uint32_t(nbox) * (SM::C_BOX + SM::N_BOX));
         const int c = kb / kChunk, jb = (kb % kChunk) / 8;
         const int y = int(int64_t(c) * a.rows_pad + r0);
-        tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES, &tm_codes, jb * kCodeBox, y, &code_full[cs]);
-        if constexpr (GF<FAM>::NIB) tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES, &tm_nib, 0, y, &code_full[cs]);
+        for (int hb = 0; hb < nbox; ++hb) {
+          tma_load_2d(smem + SM::OFF_C + cs * SM::C_BYTES + hb * SM::C_BOX, &tm_codes, jb * kCodeBox, y + hb * kBM,
+                      &code_full[cs]);
+          if constexpr (GF<FAM>::NIB)
+            tma_load_2d(smem + SM::OFF_N + cs * SM::N_BYTES + hb * SM::N_BOX, &tm_nib, 0, y + hb * kBM, &code_full[cs]);
+        }
       }
 #ifdef CCQ_GEMM_TRACE
       if (blockIdx.x == 0 && blockIdx.y < 3840 / kDecWarps) g_gtrace2[(blockIdx.y * kDecWarps) * 4 + 3] = pw;
@@ -616,7 +636,7 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
 #endif
         tc_fence_after();
         const uint64_t db_s = db_ring + uint64_t((s * SM::B_BYTES) >> 4);
-        const uint32_t ta_s = tmem_a + (s * G * SPLIT) * kACols;
+        const uint32_t ta_s = tmem_a + (s * G * RT * SPLIT) * kACols;
 #ifdef CCQ_GEMM_TRACE
         const unsigned long long tb0 = gclk();
         if (g_gexp != 2)
@@ -628,11 +648,14 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
             for (int k = 0; k < kBK / 16; ++k) {
               // A from TMEM (lane = weight row, 8 columns per K = 16);
               // B: 128B-swizzled K-major (TMA layout): 32 B per K step inside the atom.
+              // Row tile ht of the CTA: accumulator columns ht * SPLIT * BN.
               const uint64_t db = db_s + uint64_t((gg * SM::B_BLOCK + k * 32) >> 4);
 #pragma unroll
-              for (int h = 0; h < SPLIT; ++h)
-                mma_f16_ts_warp(tmem_d + h * BN, ta_s + (gg * SPLIT + h) * kACols + k * 8, db, idesc,
-                                (st | gg | k) != 0);
+              for (int ht = 0; ht < RT; ++ht)
+#pragma unroll
+                for (int h = 0; h < SPLIT; ++h)
+                  mma_f16_ts_warp(tmem_d + (ht * SPLIT + h) * BN, ta_s + ((gg * RT + ht) * SPLIT + h) * kACols + k * 8,
+                                  db, idesc, (st | gg | k) != 0);
             }
           }
         }
@@ -652,9 +675,10 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
   } else if (warp < kDecWarps) {
     // ---------------- decode producers (+ epilogue) ----------------
     const int quad = warp & 3;              // TMEM lane quadrant this warp may access
-    const int parity = warp >> 2;           // K blocks kb % kPar == parity
-    const int r = quad * 32 + lane;         // tile row == TMEM lane
-    const int64_t row = r0 + r;
+    const int ht = (warp >> 2) % RT;        // row tile of the CTA
+    const int parity = warp / (4 * RT);     // K blocks kb % kPar == parity
+    const int r = quad * 32 + lane;         // row in the tile == TMEM lane
+    const int64_t row = r0 + ht * kBM + r;
     const uint32_t lane_base = uint32_t(quad * 32) << 16;
     // Rows past row_end decode row_end-1's plan (their output is never
     // stored); an unconditional load keeps M a known 32-bit operand, so
@@ -709,11 +733,12 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
       }
 #endif
       GT(t_code);
-      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES;
+      const uint8_t* cstage = smem + SM::OFF_C + cs * SM::C_BYTES + ht * SM::C_BOX;
       uint32_t nibword = 0;
       if constexpr (FAM == kF206)
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nibword)
-                     : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + r * 16 + (((kb0 + kbs) % kChunk) / 8) * 4)));
+                     : "r"(smem_addr(smem + SM::OFF_N + cs * SM::N_BYTES + ht * SM::N_BOX + r * 16 +
+                                     (((kb0 + kbs) % kChunk) / 8) * 4)));
       // two groups in flight per warp for 2.75 / 2.5 (more ILP for their
       // shift/mask decoders: 2-4 % at M <= 64); 2.06 is issue-bound, unchanged
       // (profiles/r01_gemm_unroll2_experiment.txt)
@@ -774,8 +799,8 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
         if (acc == 0x12345678u) g_gtrace[4095 * 8] = acc;  // keep the decode alive
       } else {
 #endif
-      tmem_st32(tmem_a + lane_base + ((s * G + gg) * SPLIT) * kACols, h);
-      if constexpr (SPLIT == 2) tmem_st32(tmem_a + lane_base + ((s * G + gg) * SPLIT + 1) * kACols, h2);
+      tmem_st32(tmem_a + lane_base + (((s * G + gg) * RT + ht) * SPLIT) * kACols, h);
+      if constexpr (SPLIT == 2) tmem_st32(tmem_a + lane_base + (((s * G + gg) * RT + ht) * SPLIT + 1) * kACols, h2);
 #ifdef CCQ_GEMM_TRACE
       }
 #endif
@@ -805,10 +830,10 @@ __global__ void __launch_bounds__(Roles<PAR>::kThreads, 1)
 #pragma unroll 1
     for (int cc = parity * 32; cc < BN; cc += 32 * kPar) {
       uint32_t v[32];
-      tmem_ld32(tmem_d + lane_base + cc, v);
+      tmem_ld32(tmem_d + ht * SPLIT * BN + lane_base + cc, v);
       if constexpr (SPLIT == 2) {
         uint32_t vh[32];
-        tmem_ld32(tmem_d + BN + lane_base + cc, vh);
+        tmem_ld32(tmem_d + (ht * SPLIT + 1) * BN + lane_base + cc, vh);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(fmaf(64.f, __uint_as_float(vh[i]), __uint_as_float(v[i])));
@@ -868,11 +893,12 @@ __global__ void __launch_bounds__(256) splitk_reduce(const float* __restrict__ p
   }
 }
 
-template <int FAM, int BN, int PAR>
+template <int FAM, int BN, int PAR, int RT>
 int run_gemm_p(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void* y, int y_dtype,
                cudaStream_t s, const int32_t* offsets_dev, int64_t rows_e, int E,
                int64_t max_tokens, const int32_t* tile_prefix, int64_t max_tiles) {
-  using SM = GemmSmem<FAM, BN, PAR>;
+  using SM = GemmSmem<FAM, BN, PAR, RT>;
+  constexpr int kRows = kBM * RT;
   const int64_t K = m->cols;
   const bool grouped = offsets_dev != nullptr;
   const int xs = x_dtype == CCQ_DTYPE_F32 ? 2 : 1;
@@ -923,9 +949,9 @@ int run_gemm_p(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
     return st;
   }
   GemmArgs a{m->super, m->plan, y, y_dtype, M, m->rows, K, m->rows_pad, int(m->gpr),
-             offsets_dev, rows_e, grouped ? int((rows_e + kBM - 1) / kBM) : 0, xs, inv_scale, 0, nullptr,
+             offsets_dev, rows_e, grouped ? int((rows_e + kRows - 1) / kRows) : 0, xs, inv_scale, 0, nullptr,
              tile_prefix, E, 0, 0, 0};
-  auto kern = gemm_ccq<FAM, BN, PAR>;
+  auto kern = gemm_ccq<FAM, BN, PAR, RT>;
   if (int st2 = ensure_smem(reinterpret_cast<const void*>(kern), SM::TOTAL)) {
     cudaFreeAsync(x16, s);
     return st2;
@@ -933,7 +959,7 @@ int run_gemm_p(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
   const int tb = BN / xs;
   dim3 grid = grouped ? (tile_prefix ? dim3(unsigned(max_tiles), unsigned(a.tpe))
                                      : dim3(unsigned((max_tokens + tb - 1) / tb), unsigned(E * a.tpe)))
-                      : dim3(unsigned((M + tb - 1) / tb), unsigned((m->rows + kBM - 1) / kBM));
+                      : dim3(unsigned((M + tb - 1) / tb), unsigned((m->rows + kRows - 1) / kRows));
   // Split K when the tiles would leave most SMs idle (K-heavy shapes such as
   // 14336 -> 4096: 32 row tiles); splits cover whole 8-group code blocks.
   float* part = nullptr;
@@ -978,7 +1004,7 @@ int run_gemm_p(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
     }
   }
   if (grid.x && grid.y) {
-    cudaError_t le = launch_pdl(kern, grid, dim3(Roles<PAR>::kThreads), SM::TOTAL, s, tm_codes, tm_nib, tm_x, a);
+    cudaError_t le = launch_pdl(kern, grid, dim3(Roles<PAR, RT>::kThreads), SM::TOTAL, s, tm_codes, tm_nib, tm_x, a);
     count_launch();
     if (le == cudaSuccess && part) {
       const int64_t total = M * m->rows;
@@ -1002,8 +1028,10 @@ int run_gemm_p(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, vo
 // Decode warp groups per CTA (PAR, see groups_per_stage): CCQ_GEMM_PAR
 // overrides the default; variants are compiled where their ring fits and the
 // register budget (65536 / threads) holds the decoder without spills.
-template <int FAM, int BN, int PAR>
+template <int FAM, int BN, int PAR, int RT = 1>
 constexpr bool par_built() {
+  if constexpr (RT == 2)  // 2.06 (<= 80 registers) at the DeepSeek-like tile widths
+    return FAM == kF206 && (BN == 128 || BN == 160) && (PAR == 2 || PAR == 3) && GemmSmem<FAM, BN, PAR, RT>::OK;
   if constexpr (PAR == 3) return true;
   if constexpr (!GemmSmem<FAM, BN, PAR>::OK || BN < 128) return false;
   if constexpr (FAM == kF206) return PAR == 4 || PAR == 5 || PAR == 6;
@@ -1022,18 +1050,22 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
              cudaStream_t s, const int32_t* offsets_dev = nullptr, int64_t rows_e = 0, int E = 0,
              int64_t max_tokens = 0, const int32_t* tile_prefix = nullptr, int64_t max_tiles = 0) {
   static const int force_par = std::getenv("CCQ_GEMM_PAR") ? std::atoi(std::getenv("CCQ_GEMM_PAR")) : 0;
-  const int par = force_par > 0 ? force_par : gemm_par_default(FAM, BN);
-#define CCQ_PAR(P)                                                                                       \
-  if constexpr (par_built<FAM, BN, P>())                                                                 \
-    if (par == P)                                                                                        \
-      return run_gemm_p<FAM, BN, P>(m, x, x_dtype, M, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens, \
-                                    tile_prefix, max_tiles);
-  CCQ_PAR(4)
-  CCQ_PAR(5)
-  CCQ_PAR(6)
+  static const int force_rt = std::getenv("CCQ_GEMM_RT") ? std::atoi(std::getenv("CCQ_GEMM_RT")) : 0;
+  const int rt = force_rt > 0 ? force_rt : 1;
+  const int par = force_par > 0 ? force_par : rt == 2 ? 2 : gemm_par_default(FAM, BN);
+#define CCQ_PAR(P, R)                                                                                       \
+  if constexpr (par_built<FAM, BN, P, R>())                                                                 \
+    if (par == P && rt == R)                                                                                \
+      return run_gemm_p<FAM, BN, P, R>(m, x, x_dtype, M, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens, \
+                                       tile_prefix, max_tiles);
+  CCQ_PAR(4, 1)
+  CCQ_PAR(5, 1)
+  CCQ_PAR(6, 1)
+  CCQ_PAR(2, 2)
+  CCQ_PAR(3, 2)
 #undef CCQ_PAR
-  return run_gemm_p<FAM, BN, 3>(m, x, x_dtype, M, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens, tile_prefix,
-                                max_tiles);
+  return run_gemm_p<FAM, BN, 3, 1>(m, x, x_dtype, M, y, y_dtype, s, offsets_dev, rows_e, E, max_tokens, tile_prefix,
+                                   max_tiles);
 }
 
 }  // namespace

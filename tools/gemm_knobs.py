@@ -18,7 +18,7 @@ from paper_2507_07145_b200.synthetic import random_packed  # noqa: E402
 
 peak = float(bench.load_peaks().get("bf16_tflops", 1679.5))
 s = torch.cuda.Stream()
-knobs = {k: os.environ[k] for k in ("CCQ_GEMM_BN", "CCQ_GEMM_SPLITS", "CCQ_GROUPED_BN", "CCQ_GEMM_SK", "CCQ_GEMM_PAR") if k in os.environ}
+knobs = {k: os.environ[k] for k in ("CCQ_GEMM_BN", "CCQ_GEMM_SPLITS", "CCQ_GROUPED_BN", "CCQ_GEMM_SK", "CCQ_GEMM_PAR", "CCQ_GEMM_RT") if k in os.environ}
 if sys.argv[1] == "dense":
     fam, din, dout, M = P.FAMILIES[sys.argv[2]], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
     copies = max(2, int(160e6 // (din * dout * 0.3)) + 1)
