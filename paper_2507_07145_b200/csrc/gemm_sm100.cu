@@ -1051,7 +1051,25 @@ int run_gemm(const ccq_dev_model* m, const void* x, int x_dtype, int64_t M, void
              int64_t max_tokens = 0, const int32_t* tile_prefix = nullptr, int64_t max_tiles = 0) {
   static const int force_par = std::getenv("CCQ_GEMM_PAR") ? std::atoi(std::getenv("CCQ_GEMM_PAR")) : 0;
   static const int force_rt = std::getenv("CCQ_GEMM_RT") ? std::atoi(std::getenv("CCQ_GEMM_RT")) : 0;
-  const int rt = force_rt > 0 ? force_rt : 1;
+  // Two row tiles per CTA where they still fill the SMs: every grouped launch
+  // (many experts x row tiles) and dense grids of >= 0.8 waves at RT = 2
+  // (profiles/r02_gemm_rt.txt: DeepSeek grouped prefill 1198 -> 1120 us,
+  // 7168 -> 32768 M=128 68.4 -> 63.3 us; a one-wave 4096 -> 14336 grid at
+  // RT = 2 leaves half the SMs idle: 24.8 -> 40.0 us).
+  int rt = 1;
+  if (force_rt > 0) {
+    rt = force_rt;
+  } else if (par_built<FAM, BN, 2, 2>()) {
+    if (offsets_dev) {
+      rt = 2;
+    } else {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const int64_t tb = BN / (x_dtype == CCQ_DTYPE_F32 ? 2 : 1);
+      const int64_t tiles2 = (m->rows + 2 * kBM - 1) / (2 * kBM) * ((M + tb - 1) / tb);
+      if (tiles2 * 5 >= int64_t(num_sms(dev)) * 4) rt = 2;
+    }
+  }
   const int par = force_par > 0 ? force_par : rt == 2 ? 2 : gemm_par_default(FAM, BN);
 #define CCQ_PAR(P, R)                                                                                       \
   if constexpr (par_built<FAM, BN, P, R>())                                                                 \
