@@ -25,7 +25,13 @@ if sys.argv[1] == "dense":
     ms = [P.DeviceModel.upload(random_packed(dout, din, fam, 64, 40 + c)) for c in range(copies)]
     x = torch.randn(M, din, device="cuda").to(torch.bfloat16)
     y = torch.empty(M, dout, device="cuda")
-    us = bench._l2_cold_us(P, torch, None, s, ms, x, y)
+    kern = os.environ.get("KNOB_KERNEL")  # force a path ("gemm", ...) instead of the dispatch
+    if kern:
+        knobs["KNOB_KERNEL"] = kern
+        us = bench._graph_time_us(torch, s, lambda: [P.matmul(mm, x, out=y, stream=s, kernel=kern) for mm in ms],
+                                  reps=10) / len(ms)
+    else:
+        us = bench._l2_cold_us(P, torch, None, s, ms, x, y)
     tf = 2 * M * din * dout / us / 1e6
     print(json.dumps({"case": "dense", "family": sys.argv[2], "d_in": din, "d_out": dout, "M": M, "knobs": knobs,
                       "us": round(us, 2), "TFLOPs": round(tf, 1), "tensor_frac": round(tf / peak, 4)}))
