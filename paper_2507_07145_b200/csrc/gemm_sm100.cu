@@ -1033,7 +1033,8 @@ constexpr bool par_built() {
   if constexpr (RT == 2)  // 2.06 (<= 80 registers) at the DeepSeek-like tile widths
     return FAM == kF206 && (BN == 128 || BN == 160) && (PAR == 2 || PAR == 3) && GemmSmem<FAM, BN, PAR, RT>::OK;
   if constexpr (PAR == 3) return true;
-  if constexpr (!GemmSmem<FAM, BN, PAR>::OK) return false;
+  // (not at 64-column tiles: PAR 4-6 measured 3-10 % slower there, profiles/r02_gemm_par_small.txt)
+  if constexpr (!GemmSmem<FAM, BN, PAR>::OK || BN < 128) return false;
   if constexpr (FAM == kF206) return PAR == 4 || PAR == 5 || PAR == 6;
   if constexpr (FAM == kF275) return BN >= 160 && (PAR == 4 || PAR == 6);
   return false;
