@@ -340,6 +340,29 @@ def test_gemm_bf16_output(oracle, ccq, cuda, fam):
     assert rel_err(y.float().cpu().numpy(), want) < 4e-3  # bf16 output rounding
 
 
+@pytest.mark.parametrize("rows", [32768, 127 * 256 + 100, 127 * 256 + 200])
+@pytest.mark.parametrize("M,xdt", [(150, "bf16"), (120, "bf16"), (70, "f32")])
+def test_gemm_two_row_tile_ctas_by_default(oracle, ccq, cuda, rows, M, xdt):
+    """Dense grids that fill >= 0.8 waves with 256-row CTAs take the two-row-
+    tile GEMM by default (2.06, 128/160-column tiles, gemm_sm100.cu RT = 2),
+    including a last CTA whose second 128-row box is absent (rows % 256 = 100)
+    or partial (200)."""
+    torch = cuda
+    cols = 512
+    s = oracle.random_packed(rows, cols, 2, 64, seed=rows + M)
+    d = ccq.DeviceModel.upload(ccq.PackedModel.from_sections(s))
+    x = oracle.random_matrix(M, cols, "gaussian", 31 + M)
+    if xdt == "bf16":
+        xt = torch.from_numpy(x).to("cuda").to(torch.bfloat16)
+        x = bf16_round(x)
+    else:
+        xt = torch.from_numpy(x).to("cuda")
+    y = ccq.matmul(d, xt, kernel="gemm")
+    torch.cuda.synchronize()
+    want = oracle.gemv_batch(s, x, threads=8)
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
+
+
 # ------------------------------------------------------- grouped experts (d) --
 
 def _expert_case(oracle, fam, E, rows, cols, counts, seed):
@@ -370,6 +393,25 @@ def test_experts_single_launch_matches_per_expert_oracle(oracle, ccq, cuda, fam,
     assert rel_err(y.cpu().numpy(), wantb) < REL_TOL
     y32 = ccq.experts_matmul(ex, offs, torch.from_numpy(x).cuda())
     assert rel_err(y32.cpu().numpy(), want) < REL_TOL
+
+
+@pytest.mark.parametrize("rows", [100, 128, 300, 512])
+def test_experts_two_row_tile_ctas(oracle, ccq, cuda, rows):
+    """Grouped 2.06 launches use 256-row CTAs (RT = 2): expert row counts whose
+    last CTA has no second 128-row box (100, 300), exactly one box (128) or
+    two full boxes (512)."""
+    torch = cuda
+    counts = [150, 40, 0, 97]
+    E, cols = len(counts), 512
+    secs, offs, x, _ = _expert_case(oracle, 2, E, rows, cols, counts, seed=rows)
+    ex = ccq.Experts.upload([ccq.PackedModel.from_sections(s) for s in secs])
+    xb = torch.from_numpy(bf16_round(x)).cuda().to(torch.bfloat16)
+    want = np.zeros((int(offs[-1]), rows), np.float32)
+    for e in range(E):
+        if counts[e]:
+            want[offs[e]:offs[e + 1]] = oracle.gemv_batch(secs[e], bf16_round(x[offs[e]:offs[e + 1]]), threads=8)
+    y = ccq.experts_matmul(ex, offs, xb)
+    assert rel_err(y.cpu().numpy(), want) < REL_TOL
 
 
 @pytest.mark.parametrize("counts", [[1, 0, 0, 1, 0, 1, 1, 0], [0, 0, 3, 0, 0, 0, 0, 0], [2, 2, 2, 2, 2, 2, 2, 2],
