@@ -1032,7 +1032,8 @@ template <int FAM, int BN, int PAR, int RT = 1>
 constexpr bool par_built() {
   if constexpr (RT == 2)  // 2.06 (<= 80 registers) at the DeepSeek-like tile widths
     // (BN = 192 fits only a 2-stage ring: measured slower, profiles/r02_gemm_rt192.txt)
-    return FAM == kF206 && (BN == 128 || BN == 160) && (PAR == 2 || PAR == 3) && GemmSmem<FAM, BN, PAR, RT>::OK;
+    return ((FAM == kF206 && (BN == 128 || BN == 160)) || (FAM == kF275 && BN == 160)) && (PAR == 2 || PAR == 3) &&
+           GemmSmem<FAM, BN, PAR, RT>::OK;
   if constexpr (PAR == 3) return true;
   // (not at 64-column tiles: PAR 4-6 measured 3-10 % slower there, profiles/r02_gemm_par_small.txt)
   if constexpr (!GemmSmem<FAM, BN, PAR>::OK || BN < 128) return false;
