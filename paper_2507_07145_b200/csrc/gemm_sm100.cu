@@ -136,10 +136,36 @@ __global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __h
   const int64_t m = blockIdx.x;
   const int64_t nq = K / 4;
   float mx = 0.f;
-  for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
-    float v[4];
-    load4<XDT>(x, m * K + q * 4, v);
-    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))));
+  // 2.06 with 16-bit activations: the token row is read ONCE with 16-byte
+  // loads and kept in registers for the conversion (K <= 8 x 8 x threads);
+  // otherwise two passes (the second from L1/L2).
+  constexpr bool kCacheable = FAM == kF206 && XDT != CCQ_DTYPE_F32 && XS == 1;
+  constexpr int kCache = 8;
+  const int64_t n8 = K / 8;
+  const bool cached = kCacheable && K % 8 == 0 && n8 <= int64_t(kCache) * blockDim.x &&
+                      (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+  uint4 cv[kCacheable ? kCache : 1];
+  auto f16b = [](uint32_t h) {
+    return XDT == CCQ_DTYPE_BF16 ? __uint_as_float(h << 16) : __half2float(__ushort_as_half(uint16_t(h)));
+  };
+  if (cached) {
+#pragma unroll
+    for (int i = 0; i < (kCacheable ? kCache : 1); ++i) {
+      const int64_t q = threadIdx.x + int64_t(i) * blockDim.x;
+      if (q < n8) {
+        cv[i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + m * K + q * 8));
+        const uint32_t w[4] = {cv[i].x, cv[i].y, cv[i].z, cv[i].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          mx = fmaxf(mx, fmaxf(fabsf(f16b(w[j] & 0xFFFFu)), fabsf(f16b(w[j] >> 16))));
+      }
+    }
+  } else {
+    for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+      float v[4];
+      load4<XDT>(x, m * K + q * 4, v);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))));
+    }
   }
   __shared__ float red[8];
 #pragma unroll
@@ -155,6 +181,30 @@ __global__ void __launch_bounds__(256) x_prepass(const void* __restrict__ x, __h
   sh = sh > 126 ? 126 : (sh < -126 ? -126 : sh);
   const float scale = __int_as_float((127 + sh) << 23);
   if (threadIdx.x == 0) inv_scale[m] = __int_as_float((127 - sh) << 23);
+  if constexpr (kCacheable) {
+    if (cached) {
+      // same arithmetic as the loop below: (x3, x2/8, x1, x0/8) per 4 K, scaled
+#pragma unroll
+      for (int i = 0; i < kCache; ++i) {
+        const int64_t q = threadIdx.x + int64_t(i) * blockDim.x;
+        if (q < n8) {
+          const uint32_t w[4] = {cv[i].x, cv[i].y, cv[i].z, cv[i].w};
+          uint32_t o[4];
+#pragma unroll
+          for (int hq = 0; hq < 2; ++hq) {
+            const float v0 = f16b(w[2 * hq] & 0xFFFFu), v1 = f16b(w[2 * hq] >> 16);
+            const float v2 = f16b(w[2 * hq + 1] & 0xFFFFu), v3 = f16b(w[2 * hq + 1] >> 16);
+            const __half2 a = __floats2half2_rn(v3 * scale, v2 * scale * 0.125f);
+            const __half2 b = __floats2half2_rn(v1 * scale, v0 * scale * 0.125f);
+            o[2 * hq] = *reinterpret_cast<const uint32_t*>(&a);
+            o[2 * hq + 1] = *reinterpret_cast<const uint32_t*>(&b);
+          }
+          *reinterpret_cast<uint4*>(out + m * K + q * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+      return;
+    }
+  }
   if constexpr (FAM != kF206) {
     // 2.75 / 2.5: K position 2U + e of a group holds weight unit_wp(c, u, e)
     // (U = 8c + u) scaled by 2^-p - the order the GEMM decoders emit
